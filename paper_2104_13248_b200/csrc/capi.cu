@@ -1,0 +1,769 @@
+// capi.cu -- host side of libconebp_b200.so: the C ABI declared in
+// include/conebp_b200.h, launch planning (tile shape, TMA box, ring depth),
+// tensor-map encoding, op counting and the z-slab planner.
+//
+// The reference seams replaced here are listed in the header.  Nothing in this
+// file computes back-projection values on the host: every value comes from the
+// sm_100a kernels in bp_kernels.cuh.
+#include "../../include/conebp_b200.h"
+#include "bp_kernels.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+using namespace cbp;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int64_t g_last_plan[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  std::string m = std::string(what) + ": " + cudaGetErrorString(e);
+  return fail(e == cudaErrorMemoryAllocation ? CBP_ENOMEM : CBP_ECUDA, m);
+}
+#define CK(call, what)                       \
+  do {                                       \
+    cudaError_t e_ = (call);                 \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+  } while (0)
+
+// ---------------------------------------------------------------- tensor maps
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// ---------------------------------------------------------------- helpers
+uint64_t fnv1a(const void* data, size_t n, uint64_t h = 1469598103934665603ull) {
+  const unsigned char* b = static_cast<const unsigned char*>(data);
+  for (size_t i = 0; i < n; ++i) {
+    h ^= b[i];
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+bool mats_finite(const float* m, int64_t n) {
+  for (int64_t q = 0; q < n; ++q)
+    if (!std::isfinite(m[q])) return false;
+  return true;
+}
+
+// fast path valid for the non-hoisting rungs when every u and depth row has a
+// zero k coefficient (geometry.py:204,206); hoisting rungs always use it.
+bool fast_path_ok(const float* mats, int64_t np, int variant) {
+  if (v_hoist(variant)) return true;
+  for (int64_t s = 0; s < np; ++s)
+    if (mats[12 * s + 2] != 0.0f || mats[12 * s + 10] != 0.0f) return false;
+  return true;
+}
+
+struct Plan {
+  int cfg = 0, TX = 16, TY = 16, NW = 16, wb = 0, hb = 0, stages = 0;
+  int kind = 1;  // 0 naive, 1 tiled fast, 2 tiled general
+  size_t smem = 0;
+  float* mats_dev = nullptr;
+  int device = -1;
+};
+
+struct PlanKey {
+  int device, variant, kind_req, pad0;
+  int64_t np, nh, nw, band_v0, band_rows, nx, ny, nz, k0, nz_total;
+  uint64_t mhash;
+  bool operator<(const PlanKey& o) const {
+    return std::memcmp(this, &o, sizeof(PlanKey)) < 0;
+  }
+};
+
+std::mutex g_mu;
+std::map<PlanKey, Plan> g_plans;
+std::map<int, unsigned long long*> g_stats;  // per-device status counters [8]
+
+int get_stats(int dev, unsigned long long** out) {
+  auto it = g_stats.find(dev);
+  if (it != g_stats.end()) {
+    *out = it->second;
+    return CBP_OK;
+  }
+  unsigned long long* p = nullptr;
+  CK(cudaMalloc(&p, 8 * sizeof(unsigned long long)), "cudaMalloc(stats)");
+  CK(cudaMemset(p, 0, 8 * sizeof(unsigned long long)), "cudaMemset(stats)");
+  g_stats[dev] = p;
+  *out = p;
+  return CBP_OK;
+}
+
+// Tile configurations: {TX, TY, consumer warps, CTAs per SM}.  Lanes span 32
+// slices; each consumer warp owns TX*TY/NW columns (one register accumulator each).
+struct TileCfg {
+  int TX, TY, NW, MINB;
+};
+constexpr TileCfg kTiles[3] = {{16, 16, 16, 1}, {16, 8, 8, 2}, {8, 8, 8, 2}};
+
+template <int V, bool GEN, int C>
+const void* tiled_fn() {
+  return reinterpret_cast<const void*>(
+      &bp_tiled_kernel<V, GEN, kTiles[C].TX, kTiles[C].TY, kTiles[C].NW, kTiles[C].MINB>);
+}
+
+template <int V, bool GEN>
+const void* tiled_by_tile(int c) {
+  if (c == 0) return tiled_fn<V, GEN, 0>();
+  if (c == 1) return tiled_fn<V, GEN, 1>();
+  return tiled_fn<V, GEN, 2>();
+}
+
+const void* tiled_kernel_ptr(int variant, bool gen, int c) {
+  switch (variant) {
+    case V_BASELINE: return gen ? tiled_by_tile<V_BASELINE, true>(c) : tiled_by_tile<V_BASELINE, false>(c);
+    case V_TRANSPOSE: return gen ? tiled_by_tile<V_TRANSPOSE, true>(c) : tiled_by_tile<V_TRANSPOSE, false>(c);
+    case V_SHARE: return tiled_by_tile<V_SHARE, false>(c);
+    case V_SYMMETRY: return tiled_by_tile<V_SYMMETRY, false>(c);
+    default: return tiled_by_tile<V_SUBLINE, false>(c);  // sub-line rungs: identical arithmetic
+  }
+}
+
+const void* naive_kernel_ptr(int variant) {
+  switch (variant) {
+    case V_BASELINE: return reinterpret_cast<const void*>(&bp_naive_kernel<V_BASELINE>);
+    case V_TRANSPOSE: return reinterpret_cast<const void*>(&bp_naive_kernel<V_TRANSPOSE>);
+    case V_SHARE: return reinterpret_cast<const void*>(&bp_naive_kernel<V_SHARE>);
+    case V_SYMMETRY: return reinterpret_cast<const void*>(&bp_naive_kernel<V_SYMMETRY>);
+    default: return reinterpret_cast<const void*>(&bp_naive_kernel<V_SUBLINE>);
+  }
+}
+
+template <int V>
+void launch_footprint(dim3 g, dim3 b, cudaStream_t st, const float* mats, int np, int nw, int nh, int nx, int ny,
+                      int nz, int k0, int nzt, int TX, int TY, int tx, int ty, int tz, int astride, unsigned* hw,
+                      unsigned* hh, int nbins) {
+  bp_footprint_kernel<V><<<g, b, 0, st>>>(mats, np, nw, nh, nx, ny, nz, k0, nzt, TX, TY, tx, ty, tz, astride, hw, hh,
+                                          nbins);
+}
+
+int run_footprint(int variant, dim3 g, dim3 b, cudaStream_t st, const float* mats, int np, int nw, int nh, int nx,
+                  int ny, int nz, int k0, int nzt, int TX, int TY, int tx, int ty, int tz, int astride, unsigned* hw,
+                  unsigned* hh, int nbins) {
+  switch (variant) {
+    case V_BASELINE: launch_footprint<V_BASELINE>(g, b, st, mats, np, nw, nh, nx, ny, nz, k0, nzt, TX, TY, tx, ty, tz, astride, hw, hh, nbins); break;
+    case V_TRANSPOSE: launch_footprint<V_TRANSPOSE>(g, b, st, mats, np, nw, nh, nx, ny, nz, k0, nzt, TX, TY, tx, ty, tz, astride, hw, hh, nbins); break;
+    case V_SHARE: launch_footprint<V_SHARE>(g, b, st, mats, np, nw, nh, nx, ny, nz, k0, nzt, TX, TY, tx, ty, tz, astride, hw, hh, nbins); break;
+    case V_SYMMETRY: launch_footprint<V_SYMMETRY>(g, b, st, mats, np, nw, nh, nx, ny, nz, k0, nzt, TX, TY, tx, ty, tz, astride, hw, hh, nbins); break;
+    default: launch_footprint<V_SUBLINE>(g, b, st, mats, np, nw, nh, nx, ny, nz, k0, nzt, TX, TY, tx, ty, tz, astride, hw, hh, nbins); break;
+  }
+  return cudaGetLastError() == cudaSuccess ? CBP_OK : fail(CBP_ECUDA, "footprint kernel launch failed");
+}
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Choose tile shape, TMA box and ring depth for a problem; uploads the matrices.
+int make_plan(const PlanKey& key, const float* mats_host, cudaStream_t stream, Plan& plan) {
+  plan = Plan();
+  plan.device = key.device;
+  const int64_t n12 = key.np * 12;
+  CK(cudaMalloc(&plan.mats_dev, n12 * sizeof(float)), "cudaMalloc(mats)");
+  CK(cudaMemcpyAsync(plan.mats_dev, mats_host, n12 * sizeof(float), cudaMemcpyHostToDevice, stream), "upload mats");
+  if (key.kind_req == 0) {
+    plan.kind = 0;
+    return CBP_OK;
+  }
+  const bool gen = !fast_path_ok(mats_host, key.np, key.variant);
+  plan.kind = gen ? 2 : 1;
+
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, key.device);
+  int smem_optin = 227 * 1024;
+  cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, key.device);
+
+  // tile: the largest column tile that still gives >= 3 waves of CTAs
+  int pick = 2;
+  for (int c = 0; c < 3; ++c) {
+    const int64_t tiles = ceil_div(key.nx, kTiles[c].TX) * ceil_div(key.ny, kTiles[c].TY) * ceil_div(key.nz, 32);
+    if (tiles >= 3LL * sms * kTiles[c].MINB) {
+      pick = c;
+      break;
+    }
+  }
+  plan.cfg = pick;
+  plan.TX = kTiles[pick].TX;
+  plan.TY = kTiles[pick].TY;
+  plan.NW = kTiles[pick].NW;
+  const int tx = (int)ceil_div(key.nx, plan.TX), ty = (int)ceil_div(key.ny, plan.TY), tz = (int)ceil_div(key.nz, 32);
+
+  // footprint histograms over (tile, angle) pairs (angles subsampled on huge problems)
+  const int nbins = 1024;
+  unsigned* hist = nullptr;
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&hist), 2 * nbins * sizeof(unsigned), stream), "alloc hist");
+  CK(cudaMemsetAsync(hist, 0, 2 * nbins * sizeof(unsigned), stream), "memset hist");
+  const int64_t n_tiles = (int64_t)tx * ty * tz;
+  int astride = 1;
+  while (n_tiles * ceil_div(key.np, astride) > 40000000LL) astride *= 2;
+  const int64_t pairs = n_tiles * ceil_div(key.np, astride);
+  const int wpb = 8;
+  dim3 g((unsigned)ceil_div(pairs, wpb)), b(32 * wpb);
+  int rc = run_footprint(key.variant, g, b, stream, plan.mats_dev, (int)key.np, (int)key.nw, (int)key.nh, (int)key.nx,
+                         (int)key.ny, (int)key.nz, (int)key.k0, (int)key.nz_total, plan.TX, plan.TY, tx, ty, tz,
+                         astride, hist, hist + nbins, nbins);
+  if (rc) return rc;
+  std::vector<unsigned> h(2 * nbins);
+  CK(cudaMemcpyAsync(h.data(), hist, 2 * nbins * sizeof(unsigned), cudaMemcpyDeviceToHost, stream), "read hist");
+  CK(cudaFreeAsync(hist, stream), "free hist");
+  CK(cudaStreamSynchronize(stream), "plan sync");
+
+  auto quantile = [&](const unsigned* hh, double q) {
+    uint64_t tot = 0;
+    for (int i = 0; i < nbins; ++i) tot += hh[i];
+    if (tot == 0) return 4;
+    uint64_t acc = 0;
+    for (int i = 0; i < nbins; ++i) {
+      acc += hh[i];
+      if ((double)acc >= q * (double)tot) return std::max(i, 2);
+    }
+    return nbins - 1;
+  };
+  int wb = std::min(quantile(h.data(), 0.999), 256);
+  int hb = std::min(quantile(h.data() + nbins, 0.999), 256);
+  hb = (hb + 3) & ~3;  // TMA: inner box extent in bytes multiple of 16
+  if (hb > 256) hb = 256;
+  wb = std::max(wb, 2);
+  hb = std::max(hb, 4);
+
+  const size_t hdr_bytes = kMaxStages * sizeof(StageHdr) + 2 * kMaxStages * sizeof(uint64_t);
+  auto stage_bytes = [&](int w, int hh) { return (size_t)(((size_t)w * hh * 4 + 127) & ~(size_t)127); };
+  // ring depth within the per-CTA share of shared memory (MINB CTAs per SM)
+  const size_t budget = (size_t)(smem_optin / kTiles[pick].MINB) - 1024 - hdr_bytes;
+  int stages = (int)std::min<size_t>(kMaxStages, budget / stage_bytes(wb, hb));
+  while (stages < 3 && (wb > 8 || hb > 8)) {  // shrink the box; oversized footprints go global
+    if (hb >= wb) hb = std::max(4, ((hb * 3 / 4) + 3) & ~3); else wb = std::max(2, wb * 3 / 4);
+    stages = (int)std::min<size_t>(kMaxStages, budget / stage_bytes(wb, hb));
+  }
+  plan.wb = wb;
+  plan.hb = hb;
+  plan.stages = std::max(stages, 1);
+  plan.smem = (size_t)plan.stages * stage_bytes(wb, hb) + hdr_bytes;
+  return CBP_OK;
+}
+
+int get_plan(const PlanKey& key, const float* mats_host, cudaStream_t stream, Plan** out) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_plans.find(key);
+  if (it != g_plans.end()) {
+    *out = &it->second;
+    return CBP_OK;
+  }
+  if (g_plans.size() >= 16) {  // simple bound: drop everything on this device
+    for (auto& kv : g_plans)
+      if (kv.second.mats_dev) cudaFree(kv.second.mats_dev);
+    g_plans.clear();
+  }
+  Plan p;
+  int rc = make_plan(key, mats_host, stream, p);
+  if (rc) {
+    if (p.mats_dev) cudaFree(p.mats_dev);
+    return rc;
+  }
+  auto res = g_plans.emplace(key, p);
+  *out = &res.first->second;
+  return CBP_OK;
+}
+
+int check_dims(int64_t np, int64_t nh, int64_t nw, int64_t nx, int64_t ny, int64_t nz) {
+  if (np < 1 || nh < 2 || nw < 2 || nx < 1 || ny < 1 || nz < 1)
+    return fail(CBP_EINVAL, "dimensions must be >= 1 (detector >= 2x2)");
+  if (nh >= (1 << 23) || nw >= (1 << 23) || np >= (1 << 30) || nx >= (1 << 24) || ny >= (1 << 24) ||
+      nz >= (1 << 24))
+    return fail(CBP_EINVAL, "dimension too large for float32 index arithmetic");
+  return CBP_OK;
+}
+
+int current_device(int* dev) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return fail(CBP_ENODEV, "no CUDA device visible");
+  }
+  CK(cudaGetDevice(dev), "cudaGetDevice");
+  return CBP_OK;
+}
+
+void vol_strides(int layout, int64_t nx, int64_t ny, int64_t nz, long long& sx, long long& sy, long long& sz) {
+  if (layout == CBP_NATURAL) {  // [z][y][x]
+    sx = 1;
+    sy = nx;
+    sz = nx * ny;
+  } else {  // [x][y][z]
+    sz = 1;
+    sy = nz;
+    sx = ny * nz;
+  }
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+int cbp_version(void) { return 100; }  // 0.1.0
+
+const char* cbp_last_error(void) { return g_err.c_str(); }
+
+int cbp_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int64_t cbp_staged_pitch(int64_t rows) { return (rows + 3) & ~(int64_t)3; }
+
+int cbp_stage_projections(const float* img_dev, int img_layout, int64_t np, int64_t nh, int64_t nw, int64_t v0,
+                          int64_t rows, float* staged_dev, int64_t pitch, void* cuda_stream) {
+  if (!img_dev || !staged_dev) return fail(CBP_EINVAL, "null buffer");
+  if (np < 1 || nh < 1 || nw < 1 || v0 < 0 || rows < 1 || v0 + rows > nh || pitch < rows || (pitch & 3))
+    return fail(CBP_EINVAL, "invalid staging band / pitch");
+  if (np > 65535 && img_layout == CBP_NATURAL) return fail(CBP_EINVAL, "np > 65535 not supported");
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  if (img_layout == CBP_NATURAL) {
+    dim3 b(32, 8), g((unsigned)ceil_div(nw, 32), (unsigned)ceil_div(pitch, 32), (unsigned)np);
+    stage_natural_kernel<<<g, b, 0, st>>>(img_dev, (int)nh, (int)nw, (int)v0, (int)rows, staged_dev, (int)pitch);
+  } else if (img_layout == CBP_TRANSPOSED) {
+    const long long cols = np * nw;
+    dim3 b(32, 8), g((unsigned)ceil_div(cols, 8));
+    stage_transposed_kernel<<<g, b, 0, st>>>(img_dev, (int)nh, (int)nw, (int)v0, (int)rows, staged_dev, (int)pitch,
+                                             cols);
+  } else {
+    return fail(CBP_EINVAL, "unknown projection layout");
+  }
+  CK(cudaGetLastError(), "stage kernel launch");
+  return CBP_OK;
+}
+
+int cbp_backproject_staged(const float* staged_dev, int64_t pitch, int64_t np, int64_t nh, int64_t nw,
+                           int64_t band_v0, int64_t band_rows, const float* mats_host, float* vol_dev, int vol_layout,
+                           int64_t nx, int64_t ny, int64_t nz, int64_t k0, int64_t nz_total, int64_t s_begin,
+                           int64_t s_end, int variant, unsigned flags, void* cuda_stream) {
+  int rc = check_dims(np, nh, nw, nx, ny, nz);
+  if (rc) return rc;
+  if (!staged_dev || !mats_host || !vol_dev) return fail(CBP_EINVAL, "null buffer");
+  if (variant < 0 || variant > 5) return fail(CBP_EINVAL, "unknown kernel variant");
+  if (vol_layout != CBP_NATURAL && vol_layout != CBP_TRANSPOSED) return fail(CBP_EINVAL, "unknown volume layout");
+  if (band_v0 < 0 || band_rows < 2 || band_v0 + band_rows > nh || pitch < band_rows || (pitch & 3))
+    return fail(CBP_EINVAL, "invalid detector-row band or pitch");
+  if (k0 < 0 || nz_total < k0 + nz) return fail(CBP_EINVAL, "slab [k0, k0+nz) outside nz_total");
+  if (v_mirror(variant) && (nz_total & 1)) return fail(CBP_EINVAL, "symmetry kernels need an even nz");
+  if (s_end <= 0) s_end = np;
+  if (s_begin < 0 || s_begin > s_end || s_end > np) return fail(CBP_EINVAL, "invalid angle range");
+  if (!mats_finite(mats_host, np * 12)) return fail(CBP_EINVAL, "projection matrices contain non-finite values");
+  if (s_begin == s_end) return CBP_OK;
+  int dev;
+  rc = current_device(&dev);
+  if (rc) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+
+  PlanKey key;
+  std::memset(&key, 0, sizeof(key));
+  key.device = dev;
+  key.variant = (variant == V_PREFETCH) ? V_SUBLINE : variant;
+  key.kind_req = (flags & CBP_FLAG_NAIVE) ? 0 : 1;
+  key.np = np; key.nh = nh; key.nw = nw; key.band_v0 = band_v0; key.band_rows = band_rows;
+  key.nx = nx; key.ny = ny; key.nz = nz; key.k0 = k0; key.nz_total = nz_total;
+  key.mhash = fnv1a(mats_host, (size_t)np * 12 * sizeof(float));
+  Plan* plan = nullptr;
+  rc = get_plan(key, mats_host, st, &plan);
+  if (rc) return rc;
+  unsigned long long* stats = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    rc = get_stats(dev, &stats);
+  }
+  if (rc) return rc;
+
+  BPParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.proj = staged_dev;
+  p.mats = plan->mats_dev;
+  p.vol = vol_dev;
+  vol_strides(vol_layout, nx, ny, nz, p.vsx, p.vsy, p.vsz);
+  p.np = (int)np; p.nw = (int)nw; p.nh = (int)nh; p.pitch = (int)pitch;
+  p.band_v0 = (int)band_v0; p.band_rows = (int)band_rows;
+  p.nx = (int)nx; p.ny = (int)ny; p.nz = (int)nz; p.k0 = (int)k0; p.nz_total = (int)nz_total;
+  p.s_begin = (int)s_begin; p.s_end = (int)s_end;
+  p.stats = stats;
+
+  if (plan->kind == 0) {
+    const int64_t nvox = nx * ny * nz;
+    dim3 b(256), g((unsigned)ceil_div(nvox, 256));
+    void* args[] = {&p};
+    CK(cudaLaunchKernel(naive_kernel_ptr(key.variant), g, b, args, 0, st), "naive kernel launch");
+    int64_t lp[9] = {1, 1, 1, 0, 0, 0, (int64_t)g.x, 0, 0};
+    std::memcpy(g_last_plan, lp, sizeof(lp));
+    return CBP_OK;
+  }
+
+  // tiled TMA path
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(CBP_ECUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+  p.tiles_x = (int)ceil_div(nx, plan->TX);
+  p.tiles_y = (int)ceil_div(ny, plan->TY);
+  p.tiles_z = (int)ceil_div(nz, 32);
+  p.wb = plan->wb;
+  p.hb = plan->hb;
+  p.stages = plan->stages;
+  if (flags & CBP_FLAG_NO_SMEM) {  // every pair through the global path: make the box unusable
+    p.wb = 1;
+    p.hb = 1;
+  }
+  CUtensorMap tmap;
+  std::memset(&tmap, 0, sizeof(tmap));
+  cuuint64_t gdim[3] = {(cuuint64_t)band_rows, (cuuint64_t)nw, (cuuint64_t)np};
+  cuuint64_t gstride[2] = {(cuuint64_t)pitch * 4, (cuuint64_t)(pitch * nw) * 4};
+  cuuint32_t box[3] = {(cuuint32_t)plan->hb, (cuuint32_t)plan->wb, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult cr = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(staged_dev), gdim, gstride, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) {
+    char buf[160];
+    std::snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled failed (%d): box %dx%d pitch %lld", (int)cr, plan->wb,
+                  plan->hb, (long long)pitch);
+    return fail(CBP_ECUDA, buf);
+  }
+  const void* fn = tiled_kernel_ptr(key.variant, plan->kind == 2, plan->cfg);
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan->smem), "set smem attribute");
+  const int64_t blocks = (int64_t)p.tiles_x * p.tiles_y * p.tiles_z;
+  if (blocks > 0x7fffffffLL) return fail(CBP_EINVAL, "volume too large for one launch");
+  dim3 g((unsigned)blocks), b((plan->NW + 1) * 32);
+  void* args[] = {&tmap, &p};
+  CK(cudaLaunchKernel(fn, g, b, args, plan->smem, st), "tiled kernel launch");
+  int64_t lp[9] = {plan->TX, plan->TY, 32, plan->wb, plan->hb, plan->stages, blocks, (int64_t)plan->smem, plan->kind};
+  std::memcpy(g_last_plan, lp, sizeof(lp));
+  return CBP_OK;
+}
+
+int cbp_backproject_f32(const float* img_dev, int64_t np, int64_t nh, int64_t nw, int img_layout,
+                        const float* mats_host, float* vol_dev, int64_t nx, int64_t ny, int64_t nz, int vol_layout,
+                        int variant, unsigned flags, void* cuda_stream) {
+  int rc = check_dims(np, nh, nw, nx, ny, nz);
+  if (rc) return rc;
+  if (!img_dev) return fail(CBP_EINVAL, "null projection buffer");
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  if (img_layout == CBP_TRANSPOSED && (nh & 3) == 0) {  // already in the staging layout
+    return cbp_backproject_staged(img_dev, nh, np, nh, nw, 0, nh, mats_host, vol_dev, vol_layout, nx, ny, nz, 0, nz, 0,
+                                  np, variant, flags, cuda_stream);
+  }
+  const int64_t pitch = cbp_staged_pitch(nh);
+  float* staged = nullptr;
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&staged), (size_t)np * nw * pitch * 4, st), "alloc staging");
+  rc = cbp_stage_projections(img_dev, img_layout, np, nh, nw, 0, nh, staged, pitch, cuda_stream);
+  if (rc == CBP_OK)
+    rc = cbp_backproject_staged(staged, pitch, np, nh, nw, 0, nh, mats_host, vol_dev, vol_layout, nx, ny, nz, 0, nz, 0,
+                                np, variant, flags, cuda_stream);
+  cudaFreeAsync(staged, st);
+  return rc;
+}
+
+int cbp_backproject_host_f32(const float* img_host, int64_t np, int64_t nh, int64_t nw, int img_layout,
+                             const float* mats_host, float* vol_host, int64_t nx, int64_t ny, int64_t nz,
+                             int vol_layout, int variant, unsigned flags) {
+  int rc = check_dims(np, nh, nw, nx, ny, nz);
+  if (rc) return rc;
+  if (!img_host || !vol_host || !mats_host) return fail(CBP_EINVAL, "null buffer");
+  int dev;
+  rc = current_device(&dev);
+  if (rc) return rc;
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream create");
+  const size_t ib = (size_t)np * nh * nw * 4, vb = (size_t)nx * ny * nz * 4;
+  float *img = nullptr, *vol = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&img), ib, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&vol), vb, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(img, img_host, ib, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(vol, vol_host, vb, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) rc = cuda_fail(e, "host path: alloc/copy in");
+  if (rc == CBP_OK)
+    rc = cbp_backproject_f32(img, np, nh, nw, img_layout, mats_host, vol, nx, ny, nz, vol_layout, variant, flags, st);
+  if (rc == CBP_OK) {
+    e = cudaMemcpyAsync(vol_host, vol, vb, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) rc = cuda_fail(e, "host path: copy out");
+  }
+  if (img) cudaFreeAsync(img, st);
+  if (vol) cudaFreeAsync(vol, st);
+  e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess && rc == CBP_OK) rc = cuda_fail(e, "host path: kernel execution");
+  cudaStreamDestroy(st);
+  if (rc == CBP_OK) rc = cbp_sync_status(nullptr, nullptr);
+  return rc;
+}
+
+int cbp_sync_status(void* cuda_stream, int64_t* stats5) {
+  int dev;
+  int rc = current_device(&dev);
+  if (rc) return rc;
+  unsigned long long* d = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    rc = get_stats(dev, &d);
+  }
+  if (rc) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  unsigned long long h[8] = {0};
+  CK(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, st), "read status");
+  CK(cudaMemsetAsync(d, 0, sizeof(h), st), "reset status");
+  CK(cudaStreamSynchronize(st), "status sync");
+  if (stats5)
+    for (int q = 0; q < 5; ++q) stats5[q] = (int64_t)h[q];
+  if (h[3]) {
+    char buf[128];
+    std::snprintf(buf, sizeof buf, "%llu samples fell outside the slab's detector-row band", h[3]);
+    return fail(CBP_EBAND, buf);
+  }
+  return CBP_OK;
+}
+
+int cbp_count_ops(const float* mats_host, int64_t np, int64_t nh, int64_t nw, int64_t nx, int64_t ny, int64_t nz,
+                  int variant, int64_t nb, int64_t* out5, void* cuda_stream) {
+  int rc = check_dims(np, nh, nw, nx, ny, nz);
+  if (rc) return rc;
+  if (!mats_host || !out5) return fail(CBP_EINVAL, "null buffer");
+  if (variant < 0 || variant > 5) return fail(CBP_EINVAL, "unknown kernel variant");
+  if (variant != V_BASELINE && (nb < 1 || np % nb)) return fail(CBP_EINVAL, "nb must divide np");
+  if (v_mirror(variant) && (nz & 1)) return fail(CBP_EINVAL, "symmetry kernels need an even nz");
+  if (!mats_finite(mats_host, np * 12)) return fail(CBP_EINVAL, "projection matrices contain non-finite values");
+  int dev;
+  rc = current_device(&dev);
+  if (rc) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  float* md = nullptr;
+  unsigned long long* cnt = nullptr;
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&md), np * 12 * 4, st), "alloc");
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&cnt), 2 * 8, st), "alloc");
+  CK(cudaMemcpyAsync(md, mats_host, np * 12 * 4, cudaMemcpyHostToDevice, st), "copy");
+  CK(cudaMemsetAsync(cnt, 0, 16, st), "memset");
+  const int64_t nvox = nx * ny * nz;
+  dim3 b(256), g((unsigned)ceil_div(nvox, 256));
+  const int V = (variant == V_PREFETCH) ? V_SUBLINE : variant;
+  switch (V) {
+    case V_BASELINE: bp_count_kernel<V_BASELINE><<<g, b, 0, st>>>(md, (int)np, (int)nw, (int)nh, (int)nx, (int)ny, (int)nz, cnt); break;
+    case V_TRANSPOSE: bp_count_kernel<V_TRANSPOSE><<<g, b, 0, st>>>(md, (int)np, (int)nw, (int)nh, (int)nx, (int)ny, (int)nz, cnt); break;
+    case V_SHARE: bp_count_kernel<V_SHARE><<<g, b, 0, st>>>(md, (int)np, (int)nw, (int)nh, (int)nx, (int)ny, (int)nz, cnt); break;
+    case V_SYMMETRY: bp_count_kernel<V_SYMMETRY><<<g, b, 0, st>>>(md, (int)np, (int)nw, (int)nh, (int)nx, (int)ny, (int)nz, cnt); break;
+    default: bp_count_kernel<V_SUBLINE><<<g, b, 0, st>>>(md, (int)np, (int)nw, (int)nh, (int)nx, (int)ny, (int)nz, cnt); break;
+  }
+  CK(cudaGetLastError(), "count kernel launch");
+  unsigned long long h[2];
+  CK(cudaMemcpyAsync(h, cnt, 16, cudaMemcpyDeviceToHost, st), "read counts");
+  cudaFreeAsync(md, st);
+  cudaFreeAsync(cnt, st);
+  CK(cudaStreamSynchronize(st), "count sync");
+  const int64_t S = (int64_t)h[0], OK = (int64_t)h[1];
+  const int64_t U = nx * ny * nz * np, C = nx * ny * np, cols = nx * ny;
+  const int64_t nbat = (variant == V_BASELINE) ? 0 : np / nb;
+  const int64_t nzh = nz / 2;
+  int64_t dots, volw, projw, interp, builds = 0;
+  // closed forms of the twin's tallies (reference.py:26-290)
+  switch (variant) {
+    case V_BASELINE: dots = 3 * U; volw = 2 * S; projw = 4 * S; interp = 3 * S; break;
+    case V_TRANSPOSE: dots = 3 * U; volw = 2 * nz * nbat * cols; projw = 4 * S; interp = 3 * S; break;
+    case V_SHARE: dots = 2 * C + nz * OK; volw = 2 * nz * nbat * cols; projw = 4 * S; interp = 3 * S; break;
+    case V_SYMMETRY: dots = 2 * C + nzh * OK; volw = 4 * nzh * nbat * cols; projw = 4 * S; interp = 3 * S; break;
+    default:  // SUBLINE, SUBLINE_PREFETCH
+      dots = 2 * C + nzh * OK; volw = 4 * nzh * nbat * cols; builds = OK; projw = 2 * nh * OK; interp = nh * OK + S;
+      break;
+  }
+  out5[0] = dots; out5[1] = volw; out5[2] = projw; out5[3] = interp; out5[4] = builds;
+  return CBP_OK;
+}
+
+}  // extern "C"
+
+// ============================================================ host planning
+namespace {
+
+// float32 corner projection with the rung's formulas (host copy of the device
+// arithmetic; x86-64 float math is IEEE binary32 and is built without FMA contraction)
+inline float h_dot4(const float* m, float fi, float fj, float fk) {
+  float a = m[0] * fi;
+  float b = m[1] * fj;
+  float c = a + b;
+  float d = m[2] * fk;
+  float e = c + d;
+  return e + m[3];
+}
+inline void h_coords(const float* m, int variant, int i, int j, int kg, int nz_total, int nh, float& x, float& y,
+                     float& z) {
+  const float fi = (float)i, fj = (float)j;
+  if (v_hoist(variant)) {
+    z = h_dot4(m + 8, fi, fj, 0.0f);
+    const float F = 1.0f / z;
+    x = h_dot4(m, fi, fj, 0.0f) * F;
+    int kk = kg;
+    bool hi = false;
+    if (v_mirror(variant) && kg >= nz_total / 2) { kk = nz_total - 1 - kg; hi = true; }
+    y = h_dot4(m + 4, fi, fj, (float)kk) * F;
+    if (hi) y = (float)(nh - 1) - y;
+  } else {
+    const float fk = (float)kg;
+    z = h_dot4(m + 8, fi, fj, fk);
+    const float f = 1.0f / z;
+    x = h_dot4(m, fi, fj, fk) * f;
+    y = h_dot4(m + 4, fi, fj, fk) * f;
+  }
+}
+
+// v range [vmin, vmax] over the corners of slices [k0, k1), all angles; false if unbounded
+bool slab_vrange(const float* mats, int64_t np, int64_t nh, int64_t nw, int64_t nx, int64_t ny, int64_t nz,
+                 int variant, int64_t k0, int64_t k1, int64_t* out_v0, int64_t* out_rows) {
+  const int nzh = (int)(nz / 2);
+  std::vector<int> ks = {(int)k0, (int)(k1 - 1)};
+  if (v_mirror(variant) && k0 < nzh && k1 - 1 >= nzh) {
+    ks.push_back(nzh - 1);
+    ks.push_back(nzh);
+  }
+  int64_t lo = INT64_MAX, hi = INT64_MIN;
+  for (int64_t s = 0; s < np; ++s) {
+    const float* m = mats + 12 * s;
+    float umn = 3e38f, umx = -3e38f, vmn = 3e38f, vmx = -3e38f;
+    bool bad = false;
+    for (int ci = 0; ci < 2; ++ci)
+      for (int cj = 0; cj < 2; ++cj)
+        for (int kg : ks) {
+          float x, y, z;
+          h_coords(m, variant, ci ? (int)nx - 1 : 0, cj ? (int)ny - 1 : 0, kg, (int)nz, (int)nh, x, y, z);
+          if (!(z > 0.0f) || !std::isfinite(x) || !std::isfinite(y)) bad = true;
+          umn = std::min(umn, x); umx = std::max(umx, x);
+          vmn = std::min(vmn, y); vmx = std::max(vmx, y);
+        }
+    if (bad) {  // cannot bound: the whole detector
+      lo = 0;
+      hi = nh - 1;
+      break;
+    }
+    // anchors ix in [floor(umin)-1, floor(umax)+1] ∩ [0, nw-2]: skip angles with no column on the detector
+    const double ulo = std::max(std::floor((double)umn) - 1.0, 0.0), uhi = std::min(std::floor((double)umx) + 1.0, (double)nw - 2);
+    if (ulo > uhi) continue;
+    const double vlo = std::max(std::floor((double)vmn) - 2.0, 0.0);
+    const double vhi = std::min(std::floor((double)vmx) + 3.0, (double)nh - 1);
+    if (vlo > vhi) continue;
+    lo = std::min(lo, (int64_t)vlo);
+    hi = std::max(hi, (int64_t)vhi);
+  }
+  if (lo > hi) {
+    *out_v0 = 0;
+    *out_rows = 0;
+  } else {
+    *out_v0 = lo;
+    *out_rows = std::max<int64_t>(hi - lo + 1, 2);
+    if (*out_v0 + *out_rows > nh) *out_v0 = nh - *out_rows;
+  }
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cbp_slab_band(const float* mats_host, int64_t np, int64_t nh, int64_t nw, int64_t nx, int64_t ny, int64_t nz,
+                  int variant, int64_t k0, int64_t k1, int64_t* v0, int64_t* rows) {
+  int rc = check_dims(np, nh, nw, nx, ny, nz);
+  if (rc) return rc;
+  if (!mats_host || !v0 || !rows) return fail(CBP_EINVAL, "null buffer");
+  if (k0 < 0 || k1 > nz || k0 >= k1) return fail(CBP_EINVAL, "invalid slab range");
+  if (!mats_finite(mats_host, np * 12)) return fail(CBP_EINVAL, "projection matrices contain non-finite values");
+  slab_vrange(mats_host, np, nh, nw, nx, ny, nz, variant, k0, k1, v0, rows);
+  return CBP_OK;
+}
+
+int cbp_slab_plan(const float* mats_host, int64_t np, int64_t nh, int64_t nw, int64_t nx, int64_t ny, int64_t nz,
+                  int variant, int64_t n_ranks, int64_t align, int64_t* k_bounds, int64_t* bands) {
+  int rc = check_dims(np, nh, nw, nx, ny, nz);
+  if (rc) return rc;
+  if (!mats_host || !k_bounds || !bands) return fail(CBP_EINVAL, "null buffer");
+  if (n_ranks < 1 || align < 1) return fail(CBP_EINVAL, "n_ranks and align must be >= 1");
+  if (!mats_finite(mats_host, np * 12)) return fail(CBP_EINVAL, "projection matrices contain non-finite values");
+  const int64_t nlayers = ceil_div(nz, align);
+  // sampled-work estimate per layer on a column/angle/slice subsample
+  const int64_t sx = std::max<int64_t>(1, nx / 48), sy = std::max<int64_t>(1, ny / 48);
+  const int64_t ss = std::max<int64_t>(1, np / 48), sk = std::max<int64_t>(1, align / 4);
+  const float umax = (float)(nw - 1), vmax = (float)(nh - 1);
+  std::vector<double> cost(nlayers, 0.0);
+  for (int64_t L = 0; L < nlayers; ++L) {
+    double c = 0.0;
+    const int64_t ka = L * align, kb = std::min(nz, ka + align);
+    for (int64_t k = ka; k < kb; k += sk)
+      for (int64_t s = 0; s < np; s += ss)
+        for (int64_t j = 0; j < ny; j += sy)
+          for (int64_t i = 0; i < nx; i += sx) {
+            float x, y, z;
+            h_coords(mats_host + 12 * s, variant, (int)i, (int)j, (int)k, (int)nz, (int)nh, x, y, z);
+            const bool uok = x >= 0.0f && x < umax;
+            if (uok) c += 0.05 + ((y >= 0.0f && y < vmax) ? 1.0 : 0.0);
+          }
+    cost[L] = c * (double)sk * (double)(kb - ka) / (double)std::max<int64_t>(1, (kb - ka + sk - 1) / sk * sk) + 1e-9;
+  }
+  std::vector<double> pre(nlayers + 1, 0.0);
+  for (int64_t L = 0; L < nlayers; ++L) pre[L + 1] = pre[L] + cost[L];
+  k_bounds[0] = 0;
+  int64_t L = 0;
+  for (int64_t r = 1; r < n_ranks; ++r) {
+    const double target = pre[nlayers] * (double)r / (double)n_ranks;
+    while (L < nlayers && pre[L + 1] <= target) ++L;
+    // pick the closer boundary of the two around the target
+    int64_t cut = L;
+    if (L < nlayers && (target - pre[L]) > (pre[L + 1] - target)) cut = L + 1;
+    cut = std::max<int64_t>(cut, ceil_div(k_bounds[r - 1], align));
+    k_bounds[r] = std::min(nz, cut * align);
+  }
+  k_bounds[n_ranks] = nz;
+  for (int64_t r = 0; r < n_ranks; ++r) {
+    if (k_bounds[r + 1] <= k_bounds[r]) {
+      bands[2 * r] = 0;
+      bands[2 * r + 1] = 0;
+      continue;
+    }
+    slab_vrange(mats_host, np, nh, nw, nx, ny, nz, variant, k_bounds[r], k_bounds[r + 1], &bands[2 * r],
+                &bands[2 * r + 1]);
+  }
+  return CBP_OK;
+}
+
+int cbp_release(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  for (auto& kv : g_plans)
+    if (kv.second.mats_dev) cudaFree(kv.second.mats_dev);
+  g_plans.clear();
+  for (auto& kv : g_stats) cudaFree(kv.second);
+  g_stats.clear();
+  return CBP_OK;
+}
+
+int cbp_last_plan(int64_t* out9) {
+  if (!out9) return fail(CBP_EINVAL, "null buffer");
+  std::memcpy(out9, g_last_plan, sizeof(g_last_plan));
+  return CBP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,60 @@
+"""The C-ABI library: builds for sm_100a, loads, exports every declared symbol.
+
+No compute calls (this container has no GPU); the host-only planners are
+exercised in test_slabs.py.
+"""
+
+import re
+import subprocess
+from pathlib import Path
+
+import pytest
+
+from paper_2104_13248_b200 import _lib
+
+REPO = Path(__file__).resolve().parents[1]
+HEADER = REPO / "include" / "conebp_b200.h"
+
+
+def declared_symbols():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\*?\s+\**(cbp_\w+)\s*\(", text, flags=re.M)))
+
+
+def test_header_declares_expected_entry_points():
+    syms = declared_symbols()
+    for name in ("cbp_backproject_f32", "cbp_backproject_staged", "cbp_stage_projections", "cbp_slab_plan",
+                 "cbp_count_ops", "cbp_last_error", "cbp_version"):
+        assert name in syms
+    assert set(syms) == set(_lib.SIGNATURES), "ctypes table out of sync with include/conebp_b200.h"
+
+
+def test_library_loads_and_exports_every_symbol():
+    L = _lib.lib()
+    for name in declared_symbols():
+        assert hasattr(L, name), name
+    assert L.cbp_version() >= 100
+    assert isinstance(L.cbp_last_error(), bytes)
+
+
+def test_library_is_sm100a_native():
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+
+
+def test_device_entry_points_fail_loudly_without_gpu():
+    L = _lib.lib()
+    if L.cbp_device_count() > 0:
+        pytest.skip("a GPU is visible")
+    import numpy as np
+
+    mats = np.zeros((1, 3, 4), np.float32)
+    mats[0, 2, 3] = 1.0
+    img = np.zeros((1, 4, 4), np.float32)
+    vol = np.zeros((2, 2, 2), np.float32)
+    rc = L.cbp_backproject_host_f32(_lib.f32ptr(img), 1, 4, 4, 0, _lib.f32ptr(mats), _lib.f32ptr(vol), 2, 2, 2, 0,
+                                    0, 0)
+    assert rc == _lib.CBP_ENODEV
+    assert b"no CUDA device" in L.cbp_last_error()
