@@ -12,7 +12,9 @@ import ctypes
 from ctypes import POINTER, c_char_p, c_float, c_int, c_int64, c_uint, c_void_p
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libconebp_b200.so"
+import os
+
+LIB_PATH = Path(os.environ.get("CBP_LIB_PATH", str(Path(__file__).resolve().parent / "libconebp_b200.so")))
 
 CBP_OK = 0
 CBP_EINVAL = -1

@@ -158,20 +158,20 @@ const void* naive_kernel_ptr(int variant) {
 template <int V>
 void launch_footprint(dim3 g, dim3 b, cudaStream_t st, const float* mats, int np, int nw, int nh, int nx, int ny,
                       int nz, int k0, int nzt, int TX, int TY, int tx, int ty, int tz, int astride, unsigned* hw,
-                      unsigned* hh, int nbins) {
-  bp_footprint_kernel<V><<<g, b, 0, st>>>(mats, np, nw, nh, nx, ny, nz, k0, nzt, TX, TY, tx, ty, tz, astride, hw, hh,
-                                          nbins);
+                      unsigned* hh, int nbins, int band_v0) {
+  bp_footprint_kernel<V><<<g, b, 0, st>>>(mats, np, nw, nh, nx, ny, nz, k0, nzt, band_v0, TX, TY, tx, ty, tz, astride,
+                                          hw, hh, nbins);
 }
 
 int run_footprint(int variant, dim3 g, dim3 b, cudaStream_t st, const float* mats, int np, int nw, int nh, int nx,
                   int ny, int nz, int k0, int nzt, int TX, int TY, int tx, int ty, int tz, int astride, unsigned* hw,
-                  unsigned* hh, int nbins) {
+                  unsigned* hh, int nbins, int band_v0) {
   switch (variant) {
-    case V_BASELINE: launch_footprint<V_BASELINE>(g, b, st, mats, np, nw, nh, nx, ny, nz, k0, nzt, TX, TY, tx, ty, tz, astride, hw, hh, nbins); break;
-    case V_TRANSPOSE: launch_footprint<V_TRANSPOSE>(g, b, st, mats, np, nw, nh, nx, ny, nz, k0, nzt, TX, TY, tx, ty, tz, astride, hw, hh, nbins); break;
-    case V_SHARE: launch_footprint<V_SHARE>(g, b, st, mats, np, nw, nh, nx, ny, nz, k0, nzt, TX, TY, tx, ty, tz, astride, hw, hh, nbins); break;
-    case V_SYMMETRY: launch_footprint<V_SYMMETRY>(g, b, st, mats, np, nw, nh, nx, ny, nz, k0, nzt, TX, TY, tx, ty, tz, astride, hw, hh, nbins); break;
-    default: launch_footprint<V_SUBLINE>(g, b, st, mats, np, nw, nh, nx, ny, nz, k0, nzt, TX, TY, tx, ty, tz, astride, hw, hh, nbins); break;
+    case V_BASELINE: launch_footprint<V_BASELINE>(g, b, st, mats, np, nw, nh, nx, ny, nz, k0, nzt, TX, TY, tx, ty, tz, astride, hw, hh, nbins, band_v0); break;
+    case V_TRANSPOSE: launch_footprint<V_TRANSPOSE>(g, b, st, mats, np, nw, nh, nx, ny, nz, k0, nzt, TX, TY, tx, ty, tz, astride, hw, hh, nbins, band_v0); break;
+    case V_SHARE: launch_footprint<V_SHARE>(g, b, st, mats, np, nw, nh, nx, ny, nz, k0, nzt, TX, TY, tx, ty, tz, astride, hw, hh, nbins, band_v0); break;
+    case V_SYMMETRY: launch_footprint<V_SYMMETRY>(g, b, st, mats, np, nw, nh, nx, ny, nz, k0, nzt, TX, TY, tx, ty, tz, astride, hw, hh, nbins, band_v0); break;
+    default: launch_footprint<V_SUBLINE>(g, b, st, mats, np, nw, nh, nx, ny, nz, k0, nzt, TX, TY, tx, ty, tz, astride, hw, hh, nbins, band_v0); break;
   }
   return cudaGetLastError() == cudaSuccess ? CBP_OK : fail(CBP_ECUDA, "footprint kernel launch failed");
 }
@@ -225,7 +225,7 @@ int make_plan(const PlanKey& key, const float* mats_host, cudaStream_t stream, P
   dim3 g((unsigned)ceil_div(pairs, wpb)), b(32 * wpb);
   int rc = run_footprint(key.variant, g, b, stream, plan.mats_dev, (int)key.np, (int)key.nw, (int)key.nh, (int)key.nx,
                          (int)key.ny, (int)key.nz, (int)key.k0, (int)key.nz_total, plan.TX, plan.TY, tx, ty, tz,
-                         astride, hist, hist + nbins, nbins);
+                         astride, hist, hist + nbins, nbins, (int)key.band_v0);
   if (rc) return rc;
   std::vector<unsigned> h(2 * nbins);
   CK(cudaMemcpyAsync(h.data(), hist, 2 * nbins * sizeof(unsigned), cudaMemcpyDeviceToHost, stream), "read hist");
