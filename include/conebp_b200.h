@@ -71,6 +71,7 @@ extern "C" {
 #define CBP_FLAG_NAIVE 1u        /* one thread per voxel, global gathers (reference-simple GPU path) */
 #define CBP_FLAG_NO_SMEM 2u      /* tiled kernel, but gather from global memory (no TMA staging) */
 #define CBP_FLAG_FMA_LERP 4u     /* reserved: contract the lerps into FMA (not bit-exact) */
+#define CBP_FLAG_CHECK 8u        /* verify every shared-memory sample against the TMA box (debug) */
 
 /* Library version (major*10000 + minor*100 + patch). */
 int cbp_version(void);
@@ -79,14 +80,16 @@ const char* cbp_last_error(void);
 /* Number of visible CUDA devices (0 when none; never fails). */
 int cbp_device_count(void);
 
-/* Row pitch (in floats) of the staging layout for a band of `rows` detector rows. */
-int64_t cbp_staged_pitch(int64_t rows);
+/* Row pitch (in floats) of the staging layout for a detector `nw` pixels wide. */
+int64_t cbp_staged_pitch(int64_t nw);
 
 /*
- * Re-lay projections into the staging layout staged[s][u][r] = img[s][v0 + r][u]
- * for r in [0, rows), zero for r in [rows, pitch).  img_dev is [np][nh][nw]
- * (NATURAL) or [np][nw][nh] (TRANSPOSED).  Replaces tensors.transpose_projections
- * (tensors.py:138-147) and extracts the detector-row band [v0, v0+rows).
+ * Re-lay projections into the staging layout staged[s][r][u] = img[s][v0 + r][u]
+ * for r in [0, rows), u in [0, nw); zero for u in [nw, pitch).  img_dev is
+ * [np][nh][nw] (NATURAL) or [np][nw][nh] (TRANSPOSED).  The layout is the NATURAL
+ * one with a 16-byte row pitch, so NATURAL inputs with nw % 4 == 0 are used in
+ * place.  Replaces tensors.transpose_projections (tensors.py:138-147) for
+ * TRANSPOSED inputs and extracts the detector-row band [v0, v0+rows).
  */
 int cbp_stage_projections(const float* img_dev, int img_layout, int64_t np, int64_t nh,
                           int64_t nw, int64_t v0, int64_t rows, float* staged_dev,
@@ -104,7 +107,7 @@ int cbp_backproject_f32(const float* img_dev, int64_t np, int64_t nh, int64_t nw
 /*
  * z-slab kernel call on staged projections: vol_dev holds slices [k0, k0+nz) of a
  * volume with nz_total slices; staged_dev holds detector rows [band_v0,
- * band_v0+band_rows) in the staging layout with row pitch `pitch`.  Angles
+ * band_v0+band_rows) in the staging layout [np][band_rows][pitch].  Angles
  * [s_begin, s_end) are accumulated (s_end <= 0 means np).  Detector rows outside
  * the band that a voxel would sample raise CBP_EBAND through cbp_sync_status().
  */

@@ -28,6 +28,7 @@ TRANSPOSED = 1
 
 FLAG_NAIVE = 1
 FLAG_NO_SMEM = 2
+FLAG_CHECK = 8
 
 _f32p = POINTER(c_float)
 _i64p = POINTER(c_int64)

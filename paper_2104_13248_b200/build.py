@@ -5,7 +5,9 @@
 The library is compiled from csrc/capi.cu (+ bp_kernels.cuh) with
 ``-gencode arch=compute_100a,code=sm_100a -lineinfo`` and a static CUDA
 runtime, so the shared object only needs the NVIDIA driver at run time.
-Host code is built without FMA contraction (-ffp-contract=off): the slab
+Device code is built with -fmad=false (no contraction of separately rounded
+products and sums into FMA, including the packed f32x2 forms); host code without
+FMA contraction (-ffp-contract=off): the slab
 planner reproduces the kernels' float32 corner arithmetic on the CPU.
 """
 
@@ -28,6 +30,9 @@ NVCC_FLAGS = [
     "-gencode",
     "arch=compute_100a,code=sm_100a",
     "-lineinfo",
+    # never contract a*b+c: ptxas fuses packed mul.rn.f32x2 + add.rn.f32x2 into FFMA2
+    # unless told not to, which would break bit-exactness with the reference
+    "-fmad=false",
     "-Xcompiler",
     "-fPIC,-ffp-contract=off",
     "-shared",

@@ -81,7 +81,7 @@ bool fast_path_ok(const float* mats, int64_t np, int variant) {
 }
 
 struct Plan {
-  int cfg = 0, TX = 16, TY = 16, NW = 16, wb = 0, hb = 0, stages = 0;
+  int cfg = 0, TX = 32, TY = 16, NW = 16, wb = 0, hb = 0, stages = 0;
   int kind = 1;  // 0 naive, 1 tiled fast, 2 tiled general
   size_t smem = 0;
   float* mats_dev = nullptr;
@@ -115,34 +115,40 @@ int get_stats(int dev, unsigned long long** out) {
   return CBP_OK;
 }
 
-// Tile configurations: {TX, TY, consumer warps, CTAs per SM}.  Lanes span 32
-// slices; each consumer warp owns TX*TY/NW columns (one register accumulator each).
+// Tile configurations {consumer warps in x, in y, CTAs per SM}: a warp is 8 x 4
+// columns, a thread owns one column's 32-slice z-run.
 struct TileCfg {
-  int TX, TY, NW, MINB;
+  int NWX, NWY, MINB;
 };
-constexpr TileCfg kTiles[3] = {{16, 16, 16, 1}, {16, 8, 8, 2}, {8, 8, 8, 2}};
+constexpr TileCfg kTiles[3] = {{4, 4, 1}, {2, 4, 2}, {2, 2, 3}};
 
-template <int V, bool GEN, int C>
+template <int V, bool GEN, int C, bool CHECK>
 const void* tiled_fn() {
   return reinterpret_cast<const void*>(
-      &bp_tiled_kernel<V, GEN, kTiles[C].TX, kTiles[C].TY, kTiles[C].NW, kTiles[C].MINB>);
+      &bp_tiled_kernel<V, GEN, kTiles[C].NWX, kTiles[C].NWY, kTiles[C].MINB, CHECK>);
 }
 
-template <int V, bool GEN>
+template <int V, bool GEN, bool CHECK>
 const void* tiled_by_tile(int c) {
-  if (c == 0) return tiled_fn<V, GEN, 0>();
-  if (c == 1) return tiled_fn<V, GEN, 1>();
-  return tiled_fn<V, GEN, 2>();
+  if (c == 0) return tiled_fn<V, GEN, 0, CHECK>();
+  if (c == 1) return tiled_fn<V, GEN, 1, CHECK>();
+  return tiled_fn<V, GEN, 2, CHECK>();
 }
 
-const void* tiled_kernel_ptr(int variant, bool gen, int c) {
+template <bool CHECK>
+const void* tiled_kernel_ptr_c(int variant, bool gen, int c) {
   switch (variant) {
-    case V_BASELINE: return gen ? tiled_by_tile<V_BASELINE, true>(c) : tiled_by_tile<V_BASELINE, false>(c);
-    case V_TRANSPOSE: return gen ? tiled_by_tile<V_TRANSPOSE, true>(c) : tiled_by_tile<V_TRANSPOSE, false>(c);
-    case V_SHARE: return tiled_by_tile<V_SHARE, false>(c);
-    case V_SYMMETRY: return tiled_by_tile<V_SYMMETRY, false>(c);
-    default: return tiled_by_tile<V_SUBLINE, false>(c);  // sub-line rungs: identical arithmetic
+    case V_BASELINE: return gen ? tiled_by_tile<V_BASELINE, true, CHECK>(c) : tiled_by_tile<V_BASELINE, false, CHECK>(c);
+    case V_TRANSPOSE:
+      return gen ? tiled_by_tile<V_TRANSPOSE, true, CHECK>(c) : tiled_by_tile<V_TRANSPOSE, false, CHECK>(c);
+    case V_SHARE: return tiled_by_tile<V_SHARE, false, CHECK>(c);
+    case V_SYMMETRY: return tiled_by_tile<V_SYMMETRY, false, CHECK>(c);
+    default: return tiled_by_tile<V_SUBLINE, false, CHECK>(c);  // sub-line rungs: identical arithmetic
   }
+}
+
+const void* tiled_kernel_ptr(int variant, bool gen, int c, bool check) {
+  return check ? tiled_kernel_ptr_c<true>(variant, gen, c) : tiled_kernel_ptr_c<false>(variant, gen, c);
 }
 
 const void* naive_kernel_ptr(int variant) {
@@ -200,16 +206,17 @@ int make_plan(const PlanKey& key, const float* mats_host, cudaStream_t stream, P
   // tile: the largest column tile that still gives >= 3 waves of CTAs
   int pick = 2;
   for (int c = 0; c < 3; ++c) {
-    const int64_t tiles = ceil_div(key.nx, kTiles[c].TX) * ceil_div(key.ny, kTiles[c].TY) * ceil_div(key.nz, 32);
+    const int64_t tiles =
+        ceil_div(key.nx, 8 * kTiles[c].NWX) * ceil_div(key.ny, 4 * kTiles[c].NWY) * ceil_div(key.nz, 32);
     if (tiles >= 3LL * sms * kTiles[c].MINB) {
       pick = c;
       break;
     }
   }
   plan.cfg = pick;
-  plan.TX = kTiles[pick].TX;
-  plan.TY = kTiles[pick].TY;
-  plan.NW = kTiles[pick].NW;
+  plan.TX = 8 * kTiles[pick].NWX;
+  plan.TY = 4 * kTiles[pick].NWY;
+  plan.NW = kTiles[pick].NWX * kTiles[pick].NWY;
   const int tx = (int)ceil_div(key.nx, plan.TX), ty = (int)ceil_div(key.ny, plan.TY), tz = (int)ceil_div(key.nz, 32);
 
   // footprint histograms over (tile, angle) pairs (angles subsampled on huge problems)
@@ -243,20 +250,18 @@ int make_plan(const PlanKey& key, const float* mats_host, cudaStream_t stream, P
     }
     return nbins - 1;
   };
-  int wb = std::min(quantile(h.data(), 0.999), 256);
-  int hb = std::min(quantile(h.data() + nbins, 0.999), 256);
-  hb = (hb + 3) & ~3;  // TMA: inner box extent in bytes multiple of 16
-  if (hb > 256) hb = 256;
-  wb = std::max(wb, 2);
-  hb = std::max(hb, 4);
+  // box rows are the smem row pitch: a multiple of 32 words keeps one detector row's
+  // texels in distinct banks (and the TMA inner extent a multiple of 16 bytes)
+  int wb = std::min((quantile(h.data(), 0.999) + 31) & ~31, 256);
+  int hb = std::min(std::max(quantile(h.data() + nbins, 0.999), 2), 256);
 
   const size_t hdr_bytes = kMaxStages * sizeof(StageHdr) + 2 * kMaxStages * sizeof(uint64_t);
   auto stage_bytes = [&](int w, int hh) { return (size_t)(((size_t)w * hh * 4 + 127) & ~(size_t)127); };
   // ring depth within the per-CTA share of shared memory (MINB CTAs per SM)
   const size_t budget = (size_t)(smem_optin / kTiles[pick].MINB) - 1024 - hdr_bytes;
   int stages = (int)std::min<size_t>(kMaxStages, budget / stage_bytes(wb, hb));
-  while (stages < 3 && (wb > 8 || hb > 8)) {  // shrink the box; oversized footprints go global
-    if (hb >= wb) hb = std::max(4, ((hb * 3 / 4) + 3) & ~3); else wb = std::max(2, wb * 3 / 4);
+  while (stages < 3 && (wb > 32 || hb > 8)) {  // shrink the box; oversized footprints go global
+    if (hb >= wb || wb <= 32) hb = std::max(2, hb * 3 / 4); else wb -= 32;
     stages = (int)std::min<size_t>(kMaxStages, budget / stage_bytes(wb, hb));
   }
   plan.wb = wb;
@@ -338,23 +343,21 @@ int cbp_device_count(void) {
   return n;
 }
 
-int64_t cbp_staged_pitch(int64_t rows) { return (rows + 3) & ~(int64_t)3; }
+int64_t cbp_staged_pitch(int64_t nw) { return (nw + 3) & ~(int64_t)3; }
 
 int cbp_stage_projections(const float* img_dev, int img_layout, int64_t np, int64_t nh, int64_t nw, int64_t v0,
                           int64_t rows, float* staged_dev, int64_t pitch, void* cuda_stream) {
   if (!img_dev || !staged_dev) return fail(CBP_EINVAL, "null buffer");
-  if (np < 1 || nh < 1 || nw < 1 || v0 < 0 || rows < 1 || v0 + rows > nh || pitch < rows || (pitch & 3))
+  if (np < 1 || nh < 1 || nw < 1 || v0 < 0 || rows < 1 || v0 + rows > nh || pitch < nw || (pitch & 3))
     return fail(CBP_EINVAL, "invalid staging band / pitch");
-  if (np > 65535 && img_layout == CBP_NATURAL) return fail(CBP_EINVAL, "np > 65535 not supported");
+  if (np > 65535) return fail(CBP_EINVAL, "np > 65535 not supported by the staging kernels");
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
   if (img_layout == CBP_NATURAL) {
-    dim3 b(32, 8), g((unsigned)ceil_div(nw, 32), (unsigned)ceil_div(pitch, 32), (unsigned)np);
-    stage_natural_kernel<<<g, b, 0, st>>>(img_dev, (int)nh, (int)nw, (int)v0, (int)rows, staged_dev, (int)pitch);
+    dim3 b(128, 4), g((unsigned)std::min<int64_t>(ceil_div(pitch, 128), 8), (unsigned)ceil_div(rows, 4), (unsigned)np);
+    stage_rows_kernel<<<g, b, 0, st>>>(img_dev, (int)nh, (int)nw, (int)v0, (int)rows, staged_dev, (int)pitch);
   } else if (img_layout == CBP_TRANSPOSED) {
-    const long long cols = np * nw;
-    dim3 b(32, 8), g((unsigned)ceil_div(cols, 8));
-    stage_transposed_kernel<<<g, b, 0, st>>>(img_dev, (int)nh, (int)nw, (int)v0, (int)rows, staged_dev, (int)pitch,
-                                             cols);
+    dim3 b(32, 8), g((unsigned)ceil_div(pitch, 32), (unsigned)ceil_div(rows, 32), (unsigned)np);
+    stage_transposed_kernel<<<g, b, 0, st>>>(img_dev, (int)nh, (int)nw, (int)v0, (int)rows, staged_dev, (int)pitch);
   } else {
     return fail(CBP_EINVAL, "unknown projection layout");
   }
@@ -371,7 +374,7 @@ int cbp_backproject_staged(const float* staged_dev, int64_t pitch, int64_t np, i
   if (!staged_dev || !mats_host || !vol_dev) return fail(CBP_EINVAL, "null buffer");
   if (variant < 0 || variant > 5) return fail(CBP_EINVAL, "unknown kernel variant");
   if (vol_layout != CBP_NATURAL && vol_layout != CBP_TRANSPOSED) return fail(CBP_EINVAL, "unknown volume layout");
-  if (band_v0 < 0 || band_rows < 2 || band_v0 + band_rows > nh || pitch < band_rows || (pitch & 3))
+  if (band_v0 < 0 || band_rows < 2 || band_v0 + band_rows > nh || pitch < nw || (pitch & 3))
     return fail(CBP_EINVAL, "invalid detector-row band or pitch");
   if (k0 < 0 || nz_total < k0 + nz) return fail(CBP_EINVAL, "slab [k0, k0+nz) outside nz_total");
   if (v_mirror(variant) && (nz_total & 1)) return fail(CBP_EINVAL, "symmetry kernels need an even nz");
@@ -434,14 +437,13 @@ int cbp_backproject_staged(const float* staged_dev, int64_t pitch, int64_t np, i
   p.hb = plan->hb;
   p.stages = plan->stages;
   if (flags & CBP_FLAG_NO_SMEM) {  // every pair through the global path: make the box unusable
-    p.wb = 1;
     p.hb = 1;
   }
   CUtensorMap tmap;
   std::memset(&tmap, 0, sizeof(tmap));
-  cuuint64_t gdim[3] = {(cuuint64_t)band_rows, (cuuint64_t)nw, (cuuint64_t)np};
-  cuuint64_t gstride[2] = {(cuuint64_t)pitch * 4, (cuuint64_t)(pitch * nw) * 4};
-  cuuint32_t box[3] = {(cuuint32_t)plan->hb, (cuuint32_t)plan->wb, 1};
+  cuuint64_t gdim[3] = {(cuuint64_t)nw, (cuuint64_t)band_rows, (cuuint64_t)np};
+  cuuint64_t gstride[2] = {(cuuint64_t)pitch * 4, (cuuint64_t)(pitch * band_rows) * 4};
+  cuuint32_t box[3] = {(cuuint32_t)plan->wb, (cuuint32_t)plan->hb, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult cr = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(staged_dev), gdim, gstride, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -452,7 +454,7 @@ int cbp_backproject_staged(const float* staged_dev, int64_t pitch, int64_t np, i
                   plan->hb, (long long)pitch);
     return fail(CBP_ECUDA, buf);
   }
-  const void* fn = tiled_kernel_ptr(key.variant, plan->kind == 2, plan->cfg);
+  const void* fn = tiled_kernel_ptr(key.variant, plan->kind == 2, plan->cfg, (flags & CBP_FLAG_CHECK) != 0);
   CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan->smem), "set smem attribute");
   const int64_t blocks = (int64_t)p.tiles_x * p.tiles_y * p.tiles_z;
   if (blocks > 0x7fffffffLL) return fail(CBP_EINVAL, "volume too large for one launch");
@@ -471,13 +473,13 @@ int cbp_backproject_f32(const float* img_dev, int64_t np, int64_t nh, int64_t nw
   if (rc) return rc;
   if (!img_dev) return fail(CBP_EINVAL, "null projection buffer");
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
-  if (img_layout == CBP_TRANSPOSED && (nh & 3) == 0) {  // already in the staging layout
-    return cbp_backproject_staged(img_dev, nh, np, nh, nw, 0, nh, mats_host, vol_dev, vol_layout, nx, ny, nz, 0, nz, 0,
+  if (img_layout == CBP_NATURAL && (nw & 3) == 0) {  // already in the staging layout: zero copy
+    return cbp_backproject_staged(img_dev, nw, np, nh, nw, 0, nh, mats_host, vol_dev, vol_layout, nx, ny, nz, 0, nz, 0,
                                   np, variant, flags, cuda_stream);
   }
-  const int64_t pitch = cbp_staged_pitch(nh);
+  const int64_t pitch = cbp_staged_pitch(nw);
   float* staged = nullptr;
-  CK(cudaMallocAsync(reinterpret_cast<void**>(&staged), (size_t)np * nw * pitch * 4, st), "alloc staging");
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&staged), (size_t)np * nh * pitch * 4, st), "alloc staging");
   rc = cbp_stage_projections(img_dev, img_layout, np, nh, nw, 0, nh, staged, pitch, cuda_stream);
   if (rc == CBP_OK)
     rc = cbp_backproject_staged(staged, pitch, np, nh, nw, 0, nh, mats_host, vol_dev, vol_layout, nx, ny, nz, 0, nz, 0,

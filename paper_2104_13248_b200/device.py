@@ -38,11 +38,11 @@ def _check_tensor(t, shape, what):
 
 
 class StagedProjections:
-    """Projections re-laid into the staging layout staged[s][u][r] on the device.
+    """Projections in the device staging layout staged[s][r][u] (u pitch % 4 == 0).
 
     Holds detector rows [v0, v0+rows) of an (np, nh, nw) stack (the whole
     detector by default).  Built by cbp_stage_projections, the replacement of
-    tensors.transpose_projections (tensors.py:138-147).
+    tensors.transpose_projections (tensors.py:138-147) for TRANSPOSED inputs.
     """
 
     def __init__(self, img_dev, n_proj: int, nh: int, nw: int, layout: Layout = Layout.NATURAL, v0: int = 0,
@@ -53,8 +53,8 @@ class StagedProjections:
         _check_tensor(img_dev, shape, "projections")
         rows = nh - v0 if rows is None else rows
         self.np, self.nh, self.nw, self.v0, self.rows = n_proj, nh, nw, v0, rows
-        self.pitch = int(_lib.lib().cbp_staged_pitch(rows))
-        self.data = torch.empty((n_proj, nw, self.pitch), dtype=torch.float32, device=img_dev.device)
+        self.pitch = int(_lib.lib().cbp_staged_pitch(nw))
+        self.data = torch.empty((n_proj, rows, self.pitch), dtype=torch.float32, device=img_dev.device)
         _lib.check(_lib.lib().cbp_stage_projections(img_dev.data_ptr(), 0 if layout is Layout.NATURAL else 1, n_proj,
                                                     nh, nw, v0, rows, self.data.data_ptr(), self.pitch,
                                                     stream_handle(stream)))
@@ -65,7 +65,7 @@ class StagedProjections:
         obj = cls.__new__(cls)
         obj.np, obj.nh, obj.nw, obj.v0, obj.rows = n_proj, nh, nw, v0, rows
         obj.pitch = int(staged_dev.shape[2])
-        _check_tensor(staged_dev, (n_proj, nw, obj.pitch), "staged projections")
+        _check_tensor(staged_dev, (n_proj, rows, obj.pitch), "staged projections")
         obj.data = staged_dev
         return obj
 

@@ -4,7 +4,7 @@ The volume is split into contiguous z-slabs with cost-balanced boundaries
 (``geometry.slab_plan``); every voxel has one writer, so no
 reduction is needed.  Projections start on rank 0 (NATURAL layout, device);
 rank r receives only the detector-row band [v0_r, v0_r + rows_r) its slab
-samples, already in the staging layout [s][u][r], in angle chunks: chunk c+1
+samples, already in the staging layout [s][r][u], in angle chunks: chunk c+1
 is in flight over NVLink while chunk c is back-projected (the kernel takes an
 angle range and accumulates in ascending s, so chunking does not change a
 single bit of the result).
@@ -48,8 +48,8 @@ def plan_slabs(mats: np.ndarray, nh: int, nw: int, nx: int, ny: int, nz: int, n_
     return SlabPlan(tuple(kb), tuple(bands), int(mats.shape[0]), nh, nw, nx, ny, nz, variant)
 
 
-def pitch_of(rows: int) -> int:
-    return (max(rows, 2) + 3) & ~3
+def pitch_of(nw: int) -> int:
+    return (nw + 3) & ~3
 
 
 class CudaBackend:
@@ -60,7 +60,7 @@ class CudaBackend:
         self.device = torch.device("cuda", torch.cuda.current_device())
 
     def empty_band(self, n_proj, nw, rows):
-        return self.torch.empty((n_proj, nw, pitch_of(rows)), dtype=self.torch.float32, device=self.device)
+        return self.torch.empty((n_proj, rows, pitch_of(nw)), dtype=self.torch.float32, device=self.device)
 
     def stage_band(self, img, plan: SlabPlan, v0, rows, out):
         from . import _lib

@@ -58,3 +58,20 @@ def test_device_entry_points_fail_loudly_without_gpu():
                                     0, 0)
     assert rc == _lib.CBP_ENODEV
     assert b"no CUDA device" in L.cbp_last_error()
+
+
+def test_no_fma_contraction_in_backprojection_sass():
+    """Bit-exactness needs separately rounded products and sums: the SASS of the
+    back-projection kernels must contain no fused FFMA2 (the only FFMA allowed are the
+    explicit Newton steps inside __frcp_rn)."""
+    out = subprocess.run(["cuobjdump", "-sass", str(_lib.LIB_PATH)], capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    funcs = re.split(r"\n\s+Function : ", out.stdout)
+    checked = 0
+    for f in funcs:
+        name = f.split("\n", 1)[0]
+        if "bp_tiled_kernel" in name or "bp_naive_kernel" in name:
+            checked += 1
+            assert "FFMA2" not in f, name
+    assert checked > 0

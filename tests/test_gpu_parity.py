@@ -32,7 +32,7 @@ from paper_2104_13248_b200 import _lib
 pytestmark = pytest.mark.gpu
 
 RUNG = {n: KernelVariant[n.upper()] for n in RUNG_NAMES}
-FLAG_SETS = {"tiled": 0, "naive": _lib.FLAG_NAIVE, "tiled_global": _lib.FLAG_NO_SMEM}
+FLAG_SETS = {"tiled": 0, "naive": _lib.FLAG_NAIVE, "tiled_global": _lib.FLAG_NO_SMEM, "tiled_check": _lib.FLAG_CHECK}
 
 
 @pytest.fixture(scope="module")
@@ -72,6 +72,8 @@ def run_device(torch, img, mats, vol0, variant, img_layout, vol_layout, flags):
     D.backproject_device(ti, mats, tv, n_proj, nh, nw, nx, ny, nz, variant, img_layout, vol_layout, flags=flags)
     stats = D.sync_status()
     assert stats["band_violations"] == 0
+    if flags & _lib.FLAG_CHECK:
+        assert stats["box_misses"] == 0, "a sample fell outside its tile's TMA footprint box"
     return tv.cpu().numpy(), stats
 
 
