@@ -252,7 +252,11 @@ int make_plan(const PlanKey& key, const float* mats_host, cudaStream_t stream, P
   };
   // box rows are the smem row pitch: a multiple of 32 words keeps one detector row's
   // texels in distinct banks (and the TMA inner extent a multiple of 16 bytes)
-  int wb = std::min((quantile(h.data(), 0.999) + 31) & ~31, 256);
+  // row pitch = 16 (mod 32) words: lanes on one pixel column but adjacent rows (columns
+  // along the ray) land 16 banks apart instead of on the same bank
+  int wb = quantile(h.data(), 0.999);
+  wb = ((wb + 15) & ~31) + 16;
+  if (wb > 240) wb = 240;
   int hb = std::min(std::max(quantile(h.data() + nbins, 0.999), 2), 256);
 
   const size_t hdr_bytes = kMaxStages * sizeof(StageHdr) + 2 * kMaxStages * sizeof(uint64_t);
@@ -260,8 +264,8 @@ int make_plan(const PlanKey& key, const float* mats_host, cudaStream_t stream, P
   // ring depth within the per-CTA share of shared memory (MINB CTAs per SM)
   const size_t budget = (size_t)(smem_optin / kTiles[pick].MINB) - 1024 - hdr_bytes;
   int stages = (int)std::min<size_t>(kMaxStages, budget / stage_bytes(wb, hb));
-  while (stages < 3 && (wb > 32 || hb > 8)) {  // shrink the box; oversized footprints go global
-    if (hb >= wb || wb <= 32) hb = std::max(2, hb * 3 / 4); else wb -= 32;
+  while (stages < 3 && (wb > 48 || hb > 8)) {  // shrink the box; oversized footprints go global
+    if (hb >= wb || wb <= 48) hb = std::max(2, hb * 3 / 4); else wb -= 32;
     stages = (int)std::min<size_t>(kMaxStages, budget / stage_bytes(wb, hb));
   }
   plan.wb = wb;
