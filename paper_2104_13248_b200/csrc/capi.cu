@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -120,7 +121,8 @@ int get_stats(int dev, unsigned long long** out) {
 struct TileCfg {
   int NWX, NWY, MINB;
 };
-constexpr TileCfg kTiles[3] = {{4, 4, 1}, {2, 4, 2}, {2, 2, 3}};
+constexpr int kNumTiles = 5;
+constexpr TileCfg kTiles[kNumTiles] = {{4, 4, 1}, {2, 4, 2}, {2, 2, 3}, {4, 3, 1}, {2, 3, 2}};
 
 template <int V, bool GEN, int C, bool CHECK>
 const void* tiled_fn() {
@@ -130,9 +132,13 @@ const void* tiled_fn() {
 
 template <int V, bool GEN, bool CHECK>
 const void* tiled_by_tile(int c) {
-  if (c == 0) return tiled_fn<V, GEN, 0, CHECK>();
-  if (c == 1) return tiled_fn<V, GEN, 1, CHECK>();
-  return tiled_fn<V, GEN, 2, CHECK>();
+  switch (c) {
+    case 0: return tiled_fn<V, GEN, 0, CHECK>();
+    case 1: return tiled_fn<V, GEN, 1, CHECK>();
+    case 3: return tiled_fn<V, GEN, 3, CHECK>();
+    case 4: return tiled_fn<V, GEN, 4, CHECK>();
+    default: return tiled_fn<V, GEN, 2, CHECK>();
+  }
 }
 
 template <bool CHECK>
@@ -212,6 +218,10 @@ int make_plan(const PlanKey& key, const float* mats_host, cudaStream_t stream, P
       pick = c;
       break;
     }
+  }
+  if (const char* env = std::getenv("CBP_TILE_CFG")) {  // tuning override
+    const int forced = std::atoi(env);
+    if (forced >= 0 && forced < kNumTiles) pick = forced;
   }
   plan.cfg = pick;
   plan.TX = 8 * kTiles[pick].NWX;
@@ -305,6 +315,20 @@ int check_dims(int64_t np, int64_t nh, int64_t nw, int64_t nx, int64_t ny, int64
       nz >= (1 << 24))
     return fail(CBP_EINVAL, "dimension too large for float32 index arithmetic");
   return CBP_OK;
+}
+
+// keep freed stream-ordered allocations cached in the device's default pool (the
+// host path allocates projection-sized buffers on every call)
+void keep_pool_warm(int dev) {
+  static std::once_flag once[64];
+  if (dev < 0 || dev >= 64) return;
+  std::call_once(once[dev], [dev] {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
 }
 
 int current_device(int* dev) {
@@ -498,29 +522,73 @@ int cbp_backproject_host_f32(const float* img_host, int64_t np, int64_t nh, int6
   int rc = check_dims(np, nh, nw, nx, ny, nz);
   if (rc) return rc;
   if (!img_host || !vol_host || !mats_host) return fail(CBP_EINVAL, "null buffer");
+  if (img_layout != CBP_NATURAL && img_layout != CBP_TRANSPOSED) return fail(CBP_EINVAL, "unknown projection layout");
   int dev;
   rc = current_device(&dev);
   if (rc) return rc;
-  cudaStream_t st;
-  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream create");
-  const size_t ib = (size_t)np * nh * nw * 4, vb = (size_t)nx * ny * nz * 4;
-  float *img = nullptr, *vol = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&img), ib, st);
-  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&vol), vb, st);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(img, img_host, ib, cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(vol, vol_host, vb, cudaMemcpyHostToDevice, st);
-  if (e != cudaSuccess) rc = cuda_fail(e, "host path: alloc/copy in");
-  if (rc == CBP_OK)
-    rc = cbp_backproject_f32(img, np, nh, nw, img_layout, mats_host, vol, nx, ny, nz, vol_layout, variant, flags, st);
+  // Pipeline: projections travel host->device in angle chunks on a copy stream while
+  // the compute stream stages and back-projects the chunks already resident.  Each
+  // chunk launch accumulates angles [s0, s1) into the volume in ascending order, so
+  // the result is bitwise identical to a single launch.
+  cudaStream_t sc = nullptr, sk = nullptr;
+  CK(cudaStreamCreateWithFlags(&sc, cudaStreamNonBlocking), "stream create");
+  cudaError_t e = cudaStreamCreateWithFlags(&sk, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    cudaStreamDestroy(sc);
+    return cuda_fail(e, "stream create");
+  }
+  const size_t per_proj = (size_t)nh * nw, ib = (size_t)np * per_proj * 4, vb = (size_t)nx * ny * nz * 4;
+  const bool direct = img_layout == CBP_NATURAL && (nw & 3) == 0;  // natural layout is the staging layout
+  const int64_t pitch = cbp_staged_pitch(nw);
+  float *img = nullptr, *vol = nullptr, *staged = nullptr;
+  int64_t n_chunks = std::min<int64_t>(np, std::max<int64_t>(1, (int64_t)(ib >> 24)));  // ~16 MiB chunks
+  n_chunks = std::min<int64_t>(n_chunks, 24);
+  if (const char* env = std::getenv("CBP_HOST_CHUNKS")) n_chunks = std::max<int64_t>(1, std::min<int64_t>(np, std::atoi(env)));
+  keep_pool_warm(dev);
+  std::vector<cudaEvent_t> ev((size_t)n_chunks, nullptr);
+  e = cudaMallocAsync(reinterpret_cast<void**>(&img), ib, sk);
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&vol), vb, sk);
+  if (e == cudaSuccess && !direct)
+    e = cudaMallocAsync(reinterpret_cast<void**>(&staged), (size_t)np * nh * pitch * 4, sk);
+  for (int64_t q = 0; q < n_chunks && e == cudaSuccess; ++q) e = cudaEventCreateWithFlags(&ev[q], cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(vol, vol_host, vb, cudaMemcpyHostToDevice, sk);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(sk);  // allocations visible to the copy stream
+  if (e != cudaSuccess) rc = cuda_fail(e, "host path: allocation / volume upload");
+  for (int64_t q = 0; q < n_chunks && rc == CBP_OK; ++q) {
+    const int64_t s0 = np * q / n_chunks, s1 = np * (q + 1) / n_chunks;
+    e = cudaMemcpyAsync(img + s0 * per_proj, img_host + s0 * per_proj, (size_t)(s1 - s0) * per_proj * 4,
+                        cudaMemcpyHostToDevice, sc);
+    if (e == cudaSuccess) e = cudaEventRecord(ev[q], sc);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sk, ev[q], 0);
+    if (e != cudaSuccess) {
+      rc = cuda_fail(e, "host path: projection upload");
+      break;
+    }
+    if (direct) {
+      rc = cbp_backproject_staged(img, nw, np, nh, nw, 0, nh, mats_host, vol, vol_layout, nx, ny, nz, 0, nz, s0, s1,
+                                  variant, flags, sk);
+    } else {
+      rc = cbp_stage_projections(img + s0 * per_proj, img_layout, s1 - s0, nh, nw, 0, nh, staged + s0 * nh * pitch,
+                                 pitch, sk);
+      if (rc == CBP_OK)
+        rc = cbp_backproject_staged(staged, pitch, np, nh, nw, 0, nh, mats_host, vol, vol_layout, nx, ny, nz, 0, nz,
+                                    s0, s1, variant, flags, sk);
+    }
+  }
   if (rc == CBP_OK) {
-    e = cudaMemcpyAsync(vol_host, vol, vb, cudaMemcpyDeviceToHost, st);
+    e = cudaMemcpyAsync(vol_host, vol, vb, cudaMemcpyDeviceToHost, sk);
     if (e != cudaSuccess) rc = cuda_fail(e, "host path: copy out");
   }
-  if (img) cudaFreeAsync(img, st);
-  if (vol) cudaFreeAsync(vol, st);
-  e = cudaStreamSynchronize(st);
+  cudaStreamSynchronize(sc);
+  if (img) cudaFreeAsync(img, sk);
+  if (vol) cudaFreeAsync(vol, sk);
+  if (staged) cudaFreeAsync(staged, sk);
+  e = cudaStreamSynchronize(sk);
   if (e != cudaSuccess && rc == CBP_OK) rc = cuda_fail(e, "host path: kernel execution");
-  cudaStreamDestroy(st);
+  for (auto x : ev)
+    if (x) cudaEventDestroy(x);
+  cudaStreamDestroy(sc);
+  cudaStreamDestroy(sk);
   if (rc == CBP_OK) rc = cbp_sync_status(nullptr, nullptr);
   return rc;
 }
