@@ -213,7 +213,7 @@ int make_plan(const PlanKey& key, const float* mats_host, cudaStream_t stream, P
   int pick = 2;
   for (int c = 0; c < 3; ++c) {
     const int64_t tiles =
-        ceil_div(key.nx, 8 * kTiles[c].NWX) * ceil_div(key.ny, 4 * kTiles[c].NWY) * ceil_div(key.nz, 32);
+        ceil_div(key.nx, 8 * kTiles[c].NWX) * ceil_div(key.ny, 4 * kTiles[c].NWY) * ceil_div(key.nz, kZR);
     if (tiles >= 3LL * sms * kTiles[c].MINB) {
       pick = c;
       break;
@@ -227,7 +227,7 @@ int make_plan(const PlanKey& key, const float* mats_host, cudaStream_t stream, P
   plan.TX = 8 * kTiles[pick].NWX;
   plan.TY = 4 * kTiles[pick].NWY;
   plan.NW = kTiles[pick].NWX * kTiles[pick].NWY;
-  const int tx = (int)ceil_div(key.nx, plan.TX), ty = (int)ceil_div(key.ny, plan.TY), tz = (int)ceil_div(key.nz, 32);
+  const int tx = (int)ceil_div(key.nx, plan.TX), ty = (int)ceil_div(key.ny, plan.TY), tz = (int)ceil_div(key.nz, kZR);
 
   // footprint histograms over (tile, angle) pairs (angles subsampled on huge problems)
   const int nbins = 1024;
@@ -460,7 +460,7 @@ int cbp_backproject_staged(const float* staged_dev, int64_t pitch, int64_t np, i
   if (!enc) return fail(CBP_ECUDA, "cuTensorMapEncodeTiled unavailable from the driver");
   p.tiles_x = (int)ceil_div(nx, plan->TX);
   p.tiles_y = (int)ceil_div(ny, plan->TY);
-  p.tiles_z = (int)ceil_div(nz, 32);
+  p.tiles_z = (int)ceil_div(nz, kZR);
   p.wb = plan->wb;
   p.hb = plan->hb;
   p.stages = plan->stages;
@@ -489,7 +489,7 @@ int cbp_backproject_staged(const float* staged_dev, int64_t pitch, int64_t np, i
   dim3 g((unsigned)blocks), b((plan->NW + 1) * 32);
   void* args[] = {&tmap, &p};
   CK(cudaLaunchKernel(fn, g, b, args, plan->smem, st), "tiled kernel launch");
-  int64_t lp[9] = {plan->TX, plan->TY, 32, plan->wb, plan->hb, plan->stages, blocks, (int64_t)plan->smem, plan->kind};
+  int64_t lp[9] = {plan->TX, plan->TY, kZR, plan->wb, plan->hb, plan->stages, blocks, (int64_t)plan->smem, plan->kind};
   std::memcpy(g_last_plan, lp, sizeof(lp));
   return CBP_OK;
 }
