@@ -50,6 +50,14 @@ FP32_OPS_GENERAL = 27.0             # general matrices (jitter)
 LDS_BYTES_PER_CLK_SM = 128.0
 
 
+def ncu_traffic(workload: str):
+    p = REPO / "profiles" / "ncu_traffic.json"
+    try:
+        return json.loads(p.read_text()).get(workload, {}).get("dram_bytes")
+    except (OSError, ValueError):
+        return None
+
+
 def measured_peaks() -> dict:
     p = REPO / "MEASURED_PEAKS.json"
     if p.exists():
@@ -312,7 +320,10 @@ def main() -> None:
         comp_bytes = 8.0 * nx * ny * nz + 4.0 * n_proj * nh * nw  # volume RMW once + each texel once
         line["roofline"] = {
             "bound": "gather", "unit": "GB/s", "achieved": gath, "peak": peak, "frac": gath / peak,
-            "traffic": None,
+            "traffic": ncu_traffic(spec.name),
+            "traffic_note": "DRAM read+write bytes per launch from a committed ncu --set full capture "
+                            "(profiles/ncu_traffic.json); the gather roofline's algorithmic bytes are L1/shared "
+                            "bytes, so DRAM traffic is shown for the HBM side",
             "peak_basis": f"128 B/clk/SM x {sms} SMs x {f_mhz:.0f} MHz (SM clock measured during run); "
                           f"algorithmic 16 B/update",
             "kernel_ms": k_avg, "kernel_gups": gups_k,
