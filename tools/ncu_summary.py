@@ -51,11 +51,10 @@ for label, k in keys:
     v, u = g(k)
     print(f"| {label} (`{k}`) | {v} {u} |")
 inst = g("smsp__inst_executed.sum")[0]
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 try:
-    dram = (float(g("dram__bytes_read.sum")[0]) + float(g("dram__bytes_write.sum")[0]))
-    du = g("dram__bytes_read.sum")[1]
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(du, 1)
-    print(f"| DRAM traffic per launch (read + write) | {dram * scale / 1e6:.1f} MB |")
+    dram = sum(float(g(k)[0]) * SCALE.get(g(k)[1], 1) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+    print(f"| DRAM traffic per launch (read + write) | {dram / 1e6:.1f} MB |")
     if updates:
         print(f"| warp instructions per 32 updates | {float(inst) * 32 / updates:.1f} |")
 except ValueError:
