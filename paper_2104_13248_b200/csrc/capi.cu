@@ -121,8 +121,8 @@ int get_stats(int dev, unsigned long long** out) {
 struct TileCfg {
   int NWX, NWY, MINB;
 };
-constexpr int kNumTiles = 5;
-constexpr TileCfg kTiles[kNumTiles] = {{4, 4, 1}, {2, 4, 2}, {2, 2, 3}, {4, 3, 1}, {2, 3, 2}};
+constexpr int kNumTiles = 6;
+constexpr TileCfg kTiles[kNumTiles] = {{4, 4, 1}, {2, 4, 2}, {2, 2, 3}, {4, 3, 1}, {2, 3, 2}, {4, 5, 1}};
 
 template <int V, bool GEN, int C, bool CHECK>
 const void* tiled_fn() {
@@ -137,6 +137,7 @@ const void* tiled_by_tile(int c) {
     case 1: return tiled_fn<V, GEN, 1, CHECK>();
     case 3: return tiled_fn<V, GEN, 3, CHECK>();
     case 4: return tiled_fn<V, GEN, 4, CHECK>();
+    case 5: return tiled_fn<V, GEN, 5, CHECK>();
     default: return tiled_fn<V, GEN, 2, CHECK>();
   }
 }
