@@ -162,6 +162,20 @@ int cbp_slab_band(const float* mats_host, int64_t np, int64_t nh, int64_t nw, in
                   int64_t ny, int64_t nz, int variant, int64_t k0, int64_t k1, int64_t* v0,
                   int64_t* rows);
 
+/*
+ * Forward projection (the back-projector's adjoint): ray-driven
+ * line integrals of a NATURAL float32 volume [nz][ny][nx] through every detector pixel
+ * centre, trilinear samples at half-voxel steps times the step -- the float64 arithmetic
+ * of conebp.phantom._forward (phantom.py:134-222), bitwise identical.  views_host is
+ * np*12 doubles per projection: source xyz, detector-centre xyz, e_u xyz, e_v xyz
+ * (world units); out_dev is [np][nh][nw].  Stream-ordered.
+ * Replaces conebp.phantom.forward_project (phantom.py:225-252).
+ */
+int cbp_forward_project_f32(const float* vol_dev, int64_t nx, int64_t ny, int64_t nz,
+                            double voxel_size, const double* views_host, int64_t np, int64_t nh,
+                            int64_t nw, double pixel_pitch_u, double pixel_pitch_v, double cu,
+                            double cv, float* out_dev, void* cuda_stream);
+
 /* Release cached plans and device scratch owned by the library on this device. */
 int cbp_release(void);
 

@@ -70,6 +70,11 @@ SIGNATURES = {
         c_int,
         [_f32p, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_int, c_int64, c_int64, _i64p, _i64p],
     ),
+    "cbp_forward_project_f32": (
+        c_int,
+        [c_void_p, c_int64, c_int64, c_int64, ctypes.c_double, POINTER(ctypes.c_double), c_int64, c_int64, c_int64,
+         ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double, c_void_p, c_void_p],
+    ),
     "cbp_release": (c_int, []),
     "cbp_last_plan": (c_int, [_i64p]),
 }

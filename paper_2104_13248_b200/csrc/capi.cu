@@ -7,6 +7,7 @@
 // sm_100a kernels in bp_kernels.cuh.
 #include "../../include/conebp_b200.h"
 #include "bp_kernels.cuh"
+#include "fwd_kernels.cuh"
 
 #include <algorithm>
 #include <cmath>
@@ -822,6 +823,31 @@ int cbp_slab_plan(const float* mats_host, int64_t np, int64_t nh, int64_t nw, in
     slab_vrange(mats_host, np, nh, nw, nx, ny, nz, variant, k_bounds[r], k_bounds[r + 1], &bands[2 * r],
                 &bands[2 * r + 1]);
   }
+  return CBP_OK;
+}
+
+int cbp_forward_project_f32(const float* vol_dev, int64_t nx, int64_t ny, int64_t nz, double voxel_size,
+                            const double* views_host, int64_t np, int64_t nh, int64_t nw, double pixel_pitch_u,
+                            double pixel_pitch_v, double cu, double cv, float* out_dev, void* cuda_stream) {
+  if (!vol_dev || !views_host || !out_dev) return fail(CBP_EINVAL, "null buffer");
+  if (nx < 2 || ny < 2 || nz < 2 || np < 1 || nh < 1 || nw < 1 || !(voxel_size > 0))
+    return fail(CBP_EINVAL, "forward projection needs a volume of at least 2x2x2 and a positive voxel size");
+  int dev;
+  int rc = current_device(&dev);
+  if (rc) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  double* vd = nullptr;
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&vd), (size_t)np * 12 * sizeof(double), st), "alloc views");
+  CK(cudaMemcpyAsync(vd, views_host, (size_t)np * 12 * sizeof(double), cudaMemcpyHostToDevice, st), "upload views");
+  FwdParams fp;
+  fp.vol = vol_dev; fp.views = vd; fp.out = out_dev;
+  fp.np = (int)np; fp.nh = (int)nh; fp.nw = (int)nw; fp.nx = (int)nx; fp.ny = (int)ny; fp.nz = (int)nz;
+  fp.pu = pixel_pitch_u; fp.pv = pixel_pitch_v; fp.cu = cu; fp.cv = cv; fp.s = voxel_size;
+  const int64_t rays = np * nh * nw;
+  bp_forward_kernel<<<(unsigned)ceil_div(rays, 256), 256, 0, st>>>(fp);
+  cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(vd, st);
+  if (e != cudaSuccess) return cuda_fail(e, "forward kernel launch");
   return CBP_OK;
 }
 

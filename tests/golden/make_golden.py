@@ -159,6 +159,26 @@ def small_cases():
     print("cfg0 done", flush=True)
 
 
+def forward_cases():
+    """Reference rasterize_phantom + forward_project (phantom.py:90-252) outputs."""
+    from conebp import EllipsoidPhantom, Ellipsoid, default_phantom, forward_project, rasterize_phantom
+
+    out = {}
+    g1 = build_geometry(nx=12, ny=12, nz=12, nw=24, nh=24, np=8)
+    truth = rasterize_phantom(default_phantom(12, 12, 12, g1.voxel_size), (12, 12, 12), g1.voxel_size)
+    out["tiny_truth"] = truth.data
+    out["tiny_proj"] = forward_project(truth, g1).data
+    g2 = build_geometry(nx=16, ny=14, nz=10, nw=40, nh=28, np=7, d=30.0, D=45.0, voxel_size=1.0,
+                        angles=[0.0, 0.3, 1.0, 1.5707963267948966, 2.2, 3.141592653589793, 4.0])
+    ph = EllipsoidPhantom((Ellipsoid((1.0, -1.0, 0.5), (2.5, 1.6, 2.0), 0.8, 0.4),
+                           Ellipsoid((-1.2, 0.8, -0.5), (1.2, 1.8, 1.4), 0.5, -0.7)))
+    t2 = rasterize_phantom(ph, (16, 14, 10), 1.0)
+    out["odd_truth"] = t2.data
+    out["odd_proj"] = forward_project(t2, g2).data
+    np.savez_compressed(HERE / "forward.npz", **out)
+    print("forward:", sorted(out), flush=True)
+
+
 def big_cases():
     res = {}
     t0 = time.time()
@@ -201,5 +221,6 @@ def big_cases():
 if __name__ == "__main__":
     print("reference conebp", conebp.__version__, "from", conebp.__file__)
     small_cases()
+    forward_cases()
     if "--big" in sys.argv:
         big_cases()
