@@ -176,6 +176,18 @@ int cbp_forward_project_f32(const float* vol_dev, int64_t nx, int64_t ny, int64_
                             int64_t nw, double pixel_pitch_u, double pixel_pitch_v, double cu,
                             double cv, float* out_dev, void* cuda_stream);
 
+/*
+ * FDK pre-processing (the reference has no filter step, F5):
+ * cosine weighting D/sqrt(D^2 + ((u-cu)pu)^2 + ((v-cv)pv)^2) and row-wise spatial
+ * Ram-Lak filtering (tau = detector pitch scaled to the isocentre) of NATURAL raw
+ * projections [np][nh][nw] on the device, written into the staging layout
+ * [np][nh][pitch] that cbp_backproject_staged reads.  Zero-padded FFT convolution
+ * (cuFFT), float32.  Stream-ordered.
+ */
+int cbp_fdk_filter_f32(const float* raw_dev, int64_t np, int64_t nh, int64_t nw, double D,
+                       double pixel_pitch_u, double pixel_pitch_v, double cu, double cv,
+                       double tau, float* out_dev, int64_t pitch, void* cuda_stream);
+
 /* Release cached plans and device scratch owned by the library on this device. */
 int cbp_release(void);
 

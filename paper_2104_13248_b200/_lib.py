@@ -75,6 +75,11 @@ SIGNATURES = {
         [c_void_p, c_int64, c_int64, c_int64, ctypes.c_double, POINTER(ctypes.c_double), c_int64, c_int64, c_int64,
          ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double, c_void_p, c_void_p],
     ),
+    "cbp_fdk_filter_f32": (
+        c_int,
+        [c_void_p, c_int64, c_int64, c_int64, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+         ctypes.c_double, ctypes.c_double, c_void_p, c_int64, c_void_p],
+    ),
     "cbp_release": (c_int, []),
     "cbp_last_plan": (c_int, [_i64p]),
 }

@@ -22,7 +22,7 @@ from pathlib import Path
 HERE = Path(__file__).resolve().parent
 CSRC = HERE / "csrc"
 LIB = HERE / "libconebp_b200.so"
-SOURCES = [CSRC / "capi.cu", CSRC / "bp_kernels.cuh", CSRC / "fwd_kernels.cuh", HERE.parent / "include" / "conebp_b200.h"]
+SOURCES = [CSRC / "capi.cu", CSRC / "bp_kernels.cuh", CSRC / "fwd_kernels.cuh", CSRC / "fdk.cuh", HERE.parent / "include" / "conebp_b200.h"]
 
 NVCC_FLAGS = [
     "-O3",
@@ -38,6 +38,9 @@ NVCC_FLAGS = [
     "-shared",
     "-cudart",
     "static",
+    "-lcufft",
+    "-Xlinker",
+    "-rpath,/usr/local/cuda/lib64",
 ]
 
 

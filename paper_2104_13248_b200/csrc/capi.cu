@@ -8,6 +8,7 @@
 #include "../../include/conebp_b200.h"
 #include "bp_kernels.cuh"
 #include "fwd_kernels.cuh"
+#include "fdk.cuh"
 
 #include <algorithm>
 #include <cmath>
@@ -849,6 +850,82 @@ int cbp_forward_project_f32(const float* vol_dev, int64_t nx, int64_t ny, int64_
   cudaFreeAsync(vd, st);
   if (e != cudaSuccess) return cuda_fail(e, "forward kernel launch");
   return CBP_OK;
+}
+
+int cbp_fdk_filter_f32(const float* raw_dev, int64_t np, int64_t nh, int64_t nw, double D, double pixel_pitch_u,
+                       double pixel_pitch_v, double cu, double cv, double tau, float* out_dev, int64_t pitch,
+                       void* cuda_stream) {
+  if (!raw_dev || !out_dev) return fail(CBP_EINVAL, "null buffer");
+  if (np < 1 || nh < 1 || nw < 2 || pitch < nw || (pitch & 3) || !(D > 0) || !(tau > 0))
+    return fail(CBP_EINVAL, "invalid FDK filter arguments");
+  int dev;
+  int rc = current_device(&dev);
+  if (rc) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  int nfft = 1;
+  while (nfft < 2 * nw) nfft <<= 1;
+  const int nspec = nfft / 2 + 1;
+  // exact DFT of the zero-padded spatial Ram-Lak kernel (even, real), times tau / nfft
+  std::vector<float> Hh(nspec);
+  {
+    const double pi = 3.14159265358979323846;
+    for (int k = 0; k < nspec; ++k) {
+      double acc = 1.0 / (4.0 * tau * tau);
+      for (int n = 1; n < nfft / 2; n += 2)
+        acc += 2.0 * (-1.0 / (pi * pi * (double)n * n * tau * tau)) * std::cos(2.0 * pi * (double)k * n / nfft);
+      Hh[k] = (float)(acc * tau / nfft);
+    }
+  }
+  const long long rows_total = (long long)np * nh;
+  const long long chunk = std::max<long long>(1, std::min<long long>(rows_total, (256ll << 20) / (8ll * nfft)));
+  float *H = nullptr, *buf = nullptr;
+  cufftComplex* spec = nullptr;
+  cufftHandle fwd = 0, inv = 0;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&H), nspec * sizeof(float), st);
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&buf), (size_t)chunk * nfft * sizeof(float), st);
+  if (e == cudaSuccess)
+    e = cudaMallocAsync(reinterpret_cast<void**>(&spec), (size_t)chunk * nspec * sizeof(cufftComplex), st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(H, Hh.data(), nspec * sizeof(float), cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) rc = cuda_fail(e, "FDK filter: allocation");
+  for (long long r0 = 0; r0 < rows_total && rc == CBP_OK; r0 += chunk) {
+    const long long rows = std::min(chunk, rows_total - r0);
+    if (!fwd || rows != chunk) {  // plans for this batch size
+      if (fwd) cufftDestroy(fwd);
+      if (inv) cufftDestroy(inv);
+      fwd = inv = 0;
+      int n[1] = {nfft};
+      if (cufftPlanMany(&fwd, 1, n, nullptr, 1, nfft, nullptr, 1, nspec, CUFFT_R2C, (int)rows) != CUFFT_SUCCESS ||
+          cufftPlanMany(&inv, 1, n, nullptr, 1, nspec, nullptr, 1, nfft, CUFFT_C2R, (int)rows) != CUFFT_SUCCESS ||
+          cufftSetStream(fwd, st) != CUFFT_SUCCESS || cufftSetStream(inv, st) != CUFFT_SUCCESS) {
+        rc = fail(CBP_ECUDA, "FDK filter: cuFFT plan creation failed");
+        break;
+      }
+    }
+    const int gz = 1024;
+    dim3 b(256), g((unsigned)std::min<long long>(ceil_div(nfft, 256), 16), (unsigned)ceil_div(rows, gz), gz);
+    fdk_weight_pad_kernel<<<g, b, 0, st>>>(raw_dev + r0 * nw, (int)nh, (int)nw, nfft, rows, r0, D, pixel_pitch_u,
+                                           pixel_pitch_v, cu, cv, buf);
+    if (cufftExecR2C(fwd, buf, spec) != CUFFT_SUCCESS) {
+      rc = fail(CBP_ECUDA, "FDK filter: cufftExecR2C failed");
+      break;
+    }
+    const long long ns = rows * nspec;
+    fdk_spectrum_kernel<<<(unsigned)ceil_div(ns, 256), 256, 0, st>>>(spec, H, nspec, rows);
+    if (cufftExecC2R(inv, spec, buf) != CUFFT_SUCCESS) {
+      rc = fail(CBP_ECUDA, "FDK filter: cufftExecC2R failed");
+      break;
+    }
+    dim3 g2((unsigned)std::min<long long>(ceil_div(pitch, 256), 16), (unsigned)ceil_div(rows, gz), gz);
+    fdk_crop_kernel<<<g2, b, 0, st>>>(buf, nfft, (int)nw, (int)pitch, rows, out_dev + r0 * pitch);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) rc = cuda_fail(e, "FDK filter: kernel launch");
+  }
+  if (fwd) cufftDestroy(fwd);
+  if (inv) cufftDestroy(inv);
+  if (H) cudaFreeAsync(H, st);
+  if (buf) cudaFreeAsync(buf, st);
+  if (spec) cudaFreeAsync(spec, st);
+  return rc;
 }
 
 int cbp_release(void) {
