@@ -126,6 +126,16 @@ struct TileCfg {
 constexpr int kNumTiles = 6;
 constexpr TileCfg kTiles[kNumTiles] = {{4, 4, 1}, {2, 4, 2}, {2, 2, 3}, {4, 3, 1}, {2, 3, 2}, {4, 5, 1}};
 
+template <int C>
+using RolesC = WarpRoles<kTiles[C].NWX * kTiles[C].NWY, kTiles[C].MINB>;
+constexpr int kTileThreads[kNumTiles] = {RolesC<0>::kThreads, RolesC<1>::kThreads, RolesC<2>::kThreads,
+                                         RolesC<3>::kThreads, RolesC<4>::kThreads, RolesC<5>::kThreads};
+// launch register allocation the setmaxnreg split assumes (0: no register reallocation)
+constexpr int kTilePool[kNumTiles] = {
+    RolesC<0>::kRealloc ? RolesC<0>::kRegLaunch : 0, RolesC<1>::kRealloc ? RolesC<1>::kRegLaunch : 0,
+    RolesC<2>::kRealloc ? RolesC<2>::kRegLaunch : 0, RolesC<3>::kRealloc ? RolesC<3>::kRegLaunch : 0,
+    RolesC<4>::kRealloc ? RolesC<4>::kRegLaunch : 0, RolesC<5>::kRealloc ? RolesC<5>::kRegLaunch : 0};
+
 template <int V, bool GEN, int C, bool CHECK>
 const void* tiled_fn() {
   return reinterpret_cast<const void*>(
@@ -267,8 +277,10 @@ int make_plan(const PlanKey& key, const float* mats_host, cudaStream_t stream, P
   // texels in distinct banks (and the TMA inner extent a multiple of 16 bytes)
   // row pitch = 16 (mod 32) words: lanes on one pixel column but adjacent rows (columns
   // along the ray) land 16 banks apart instead of on the same bank
+  int pad = 16;
+  if (const char* e = std::getenv("CBP_BOX_PAD")) pad = std::atoi(e) & 28;
   int wb = quantile(h.data(), 0.999);
-  wb = ((wb + 15) & ~31) + 16;
+  wb = ((wb - pad + 31) & ~31) + pad;
   if (wb > 240) wb = 240;
   int hb = std::min(std::max(quantile(h.data() + nbins, 0.999), 2), 256);
 
@@ -489,7 +501,17 @@ int cbp_backproject_staged(const float* staged_dev, int64_t pitch, int64_t np, i
   CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan->smem), "set smem attribute");
   const int64_t blocks = (int64_t)p.tiles_x * p.tiles_y * p.tiles_z;
   if (blocks > 0x7fffffffLL) return fail(CBP_EINVAL, "volume too large for one launch");
-  dim3 g((unsigned)blocks), b((plan->NW + 1) * 32);
+  if (kTilePool[plan->cfg] != 0) {  // setmaxnreg.inc would wait forever on a smaller pool
+    cudaFuncAttributes fa{};
+    CK(cudaFuncGetAttributes(&fa, fn), "cudaFuncGetAttributes(tiled kernel)");
+    if (fa.numRegs != kTilePool[plan->cfg]) {
+      char buf[128];
+      std::snprintf(buf, sizeof buf, "tiled kernel register pool %d != %d assumed by its setmaxnreg split",
+                    fa.numRegs, kTilePool[plan->cfg]);
+      return fail(CBP_ECUDA, buf);
+    }
+  }
+  dim3 g((unsigned)blocks), b(kTileThreads[plan->cfg]);
   void* args[] = {&tmap, &p};
   CK(cudaLaunchKernel(fn, g, b, args, plan->smem, st), "tiled kernel launch");
   int64_t lp[9] = {plan->TX, plan->TY, kZR, plan->wb, plan->hb, plan->stages, blocks, (int64_t)plan->smem, plan->kind};
