@@ -45,7 +45,8 @@ sys.path.insert(0, str(REPO))
 
 METRIC = "GUPS (voxel*projection updates/s)"
 GATHER_BYTES_PER_UPDATE = 16.0      # 4 float32 texels per bilinear sample
-FP32_OPS_FAST = 13.0                # FP32-pipe lane ops per update, vertical-column fast path
+FP32_OPS_FAST = 16.0                # FP32 lane ops per update executed by the fast hot loop: y 3, frac 1,
+                                    # blend 10, accumulate 2 (SASS: 16 FADD2/FMUL2 per slice pair)
 FP32_OPS_GENERAL = 27.0             # general matrices (jitter)
 LDS_BYTES_PER_CLK_SM = 128.0
 
