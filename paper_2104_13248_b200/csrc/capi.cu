@@ -295,6 +295,7 @@ int make_plan(const PlanKey& key, const float* mats_host, cudaStream_t stream, P
   }
   plan.wb = wb;
   plan.hb = hb;
+  if (const char* e = std::getenv("CBP_MAX_STAGES")) stages = std::min(stages, std::max(1, std::atoi(e)));  // tuning
   plan.stages = std::max(stages, 1);
   plan.smem = (size_t)plan.stages * stage_bytes(wb, hb) + hdr_bytes;
   return CBP_OK;
