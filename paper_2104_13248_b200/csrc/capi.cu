@@ -204,7 +204,7 @@ int run_footprint(int variant, dim3 g, dim3 b, cudaStream_t st, const float* mat
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // Choose tile shape, TMA box and ring depth for a problem; uploads the matrices.
-int make_plan(const PlanKey& key, const float* mats_host, cudaStream_t stream, Plan& plan) {
+int make_plan(const PlanKey& key, const float* mats_host, cudaStream_t stream, Plan& plan, int forced_cfg = -1) {
   plan = Plan();
   plan.device = key.device;
   const int64_t n12 = key.np * 12;
@@ -232,9 +232,15 @@ int make_plan(const PlanKey& key, const float* mats_host, cudaStream_t stream, P
       break;
     }
   }
+  bool may_split = pick == 0;  // candidate for two CTAs of 8 warps per SM (cfg 1), see below
   if (const char* env = std::getenv("CBP_TILE_CFG")) {  // tuning override
     const int forced = std::atoi(env);
     if (forced >= 0 && forced < kNumTiles) pick = forced;
+    may_split = false;
+  }
+  if (forced_cfg >= 0) {
+    pick = forced_cfg;
+    may_split = false;
   }
   plan.cfg = pick;
   plan.TX = 8 * kTiles[pick].NWX;
@@ -261,6 +267,21 @@ int make_plan(const PlanKey& key, const float* mats_host, cudaStream_t stream, P
   CK(cudaMemcpyAsync(h.data(), hist, 2 * nbins * sizeof(unsigned), cudaMemcpyDeviceToHost, stream), "read hist");
   CK(cudaFreeAsync(hist, stream), "free hist");
   CK(cudaStreamSynchronize(stream), "plan sync");
+
+  // One CTA of 16 consumer warps per SM (cfg 0) or two CTAs of 8 (cfg 1, 16x16 columns)?
+  // Two CTAs hide each other's ring stalls and CTA turnover (cfg1 +4%, cfg2 +2%), but
+  // double the producer work per voxel, which costs when many (tile, angle) pairs miss
+  // the detector (cfg3 30% / cfg4 67% missed: -6% / -9%).  Measured on B200, round 1.
+  if (may_split) {
+    uint64_t sampled = 0;
+    for (int i = 0; i < nbins; ++i) sampled += h[i];
+    const double missed = 1.0 - (double)sampled / (double)std::max<int64_t>(1, pairs);
+    if (missed < 0.25) {
+      cudaFree(plan.mats_dev);
+      plan.mats_dev = nullptr;
+      return make_plan(key, mats_host, stream, plan, 1);
+    }
+  }
 
   auto quantile = [&](const unsigned* hh, double q) {
     uint64_t tot = 0;
