@@ -280,3 +280,27 @@ def test_band_violation_is_reported(torch_cuda):
     D.backproject_staged(staged, g["mats"], vol, 32, 32, 8, k0=12, nz_total=32)
     with pytest.raises(CbpError):
         D.sync_status()
+
+
+@pytest.mark.parametrize("tile_cfg", range(6))
+def test_every_tile_shape_bitwise(torch_cuda, tile_cfg):
+    """Every tile shape the planner can pick (one or two CTAs per SM, 8..20 consumer
+    warps) reproduces the reference's config-1 bits, and the general (tilted-matrix)
+    path its config-2 bits: the tile shape never changes a voxel's addition chain."""
+    import os
+    import subprocess
+    import sys
+
+    ref = big_sha()
+    if ref is None:
+        pytest.skip("big_sha.json not generated")
+    here = GOLDEN.parent
+    cases = ["cfg1"] + (["cfg2"] if tile_cfg in (0, 1) and (GOLDEN / "cfg2_mats.npy").exists() else [])
+    for case in cases:
+        env = dict(os.environ, CBP_TILE_CFG=str(tile_cfg))
+        out = subprocess.run([sys.executable, str(here / "tile_case.py"), case], env=env, capture_output=True,
+                             text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        digest = out.stdout.split()[0]
+        want = ref["cfg1_uniform11" if case == "cfg1" else "cfg2_uniform12"]["baseline"]
+        assert digest == want, (case, tile_cfg, out.stdout)
