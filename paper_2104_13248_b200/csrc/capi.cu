@@ -826,37 +826,78 @@ int cbp_slab_plan(const float* mats_host, int64_t np, int64_t nh, int64_t nw, in
   if (n_ranks < 1 || align < 1) return fail(CBP_EINVAL, "n_ranks and align must be >= 1");
   if (!mats_finite(mats_host, np * 12)) return fail(CBP_EINVAL, "projection matrices contain non-finite values");
   const int64_t nlayers = ceil_div(nz, align);
-  // sampled-work estimate per layer on a column/angle/slice subsample
-  const int64_t sx = std::max<int64_t>(1, nx / 48), sy = std::max<int64_t>(1, ny / 48);
-  const int64_t ss = std::max<int64_t>(1, np / 48), sk = std::max<int64_t>(1, align / 4);
-  const float umax = (float)(nw - 1), vmax = (float)(nh - 1);
+  // Cost per layer of `align` slices, modelled on what the tiled kernel does: a (tile,
+  // angle) pair whose footprint misses the detector is never queued (cost ~ the producer's
+  // footprint test), any other pair costs the whole tile's z-run -- even when only some
+  // of its voxels are sampled -- and a little more when it crosses the detector's top or
+  // bottom row (guarded loop).  Evaluated with the kernel's corner test on a subsample of
+  // 32x16-column tiles and angles.  (A per-voxel sampled count under-weights the
+  // partially sampled tiles at the volume's z ends: 0.78 instead of 0.97 compute balance
+  // on cfg4 at 8 ranks, tools/slab_balance.py.)
+  const int64_t TXm = 32, TYm = 16;
+  const int64_t ntx = ceil_div(nx, TXm), nty = ceil_div(ny, TYm);
+  const int64_t stx = std::max<int64_t>(1, ntx / 12), sty = std::max<int64_t>(1, nty / 12);
+  const int64_t ss = std::max<int64_t>(1, np / 96);
   std::vector<double> cost(nlayers, 0.0);
   for (int64_t L = 0; L < nlayers; ++L) {
     double c = 0.0;
-    const int64_t ka = L * align, kb = std::min(nz, ka + align);
-    for (int64_t k = ka; k < kb; k += sk)
-      for (int64_t s = 0; s < np; s += ss)
-        for (int64_t j = 0; j < ny; j += sy)
-          for (int64_t i = 0; i < nx; i += sx) {
+    const int ka = (int)(L * align), kb = (int)(std::min(nz, (L + 1) * align) - 1);
+    for (int64_t s = 0; s < np; s += ss)
+      for (int64_t by = 0; by < nty; by += sty)
+        for (int64_t bx = 0; bx < ntx; bx += stx) {
+          const int i0 = (int)(bx * TXm), i1 = (int)std::min(nx, (bx + 1) * TXm) - 1;
+          const int j0 = (int)(by * TYm), j1 = (int)std::min(ny, (by + 1) * TYm) - 1;
+          float umin = 3e38f, umax_ = -3e38f, vmin = 3e38f, vmax_ = -3e38f;
+          bool bad = false;
+          int kc[4] = {ka, kb, (int)(nz / 2) - 1, (int)(nz / 2)};
+          const int nk = (v_mirror(variant) && ka < nz / 2 && kb >= nz / 2) ? 4 : 2;
+          for (int q = 0; q < 4 * nk; ++q) {
             float x, y, z;
-            h_coords(mats_host + 12 * s, variant, (int)i, (int)j, (int)k, (int)nz, (int)nh, x, y, z);
-            const bool uok = x >= 0.0f && x < umax;
-            if (uok) c += 0.05 + ((y >= 0.0f && y < vmax) ? 1.0 : 0.0);
+            h_coords(mats_host + 12 * s, variant, (q & 1) ? i1 : i0, (q & 2) ? j1 : j0, kc[q >> 2], (int)nz, (int)nh,
+                     x, y, z);
+            bad = bad || !(z > 0.0f) || !std::isfinite(x) || !std::isfinite(y);
+            umin = std::min(umin, x); umax_ = std::max(umax_, x);
+            vmin = std::min(vmin, y); vmax_ = std::max(vmax_, y);
           }
-    cost[L] = c * (double)sk * (double)(kb - ka) / (double)std::max<int64_t>(1, (kb - ka + sk - 1) / sk * sk) + 1e-9;
+          if (bad) { c += 1.0; continue; }
+          const double ulo = std::floor(umin) - 1, uhi = std::floor(umax_) + 1;
+          const double vlo = std::floor(vmin) - 1, vhi = std::floor(vmax_) + 1;
+          const bool hit = std::max(ulo, 0.0) <= std::min(uhi, (double)(nw - 2)) &&
+                           std::max(vlo, 0.0) <= std::min(vhi, (double)(nh - 2));
+          if (!hit) { c += 0.03; continue; }
+          const bool rows_inside = vlo >= 0 && vhi <= (double)(nh - 2);
+          c += rows_inside ? 1.0 : 1.15;
+        }
+    cost[L] = c * (double)(kb - ka + 1) / (double)align + 1e-9;
   }
   std::vector<double> pre(nlayers + 1, 0.0);
   for (int64_t L = 0; L < nlayers; ++L) pre[L + 1] = pre[L] + cost[L];
-  k_bounds[0] = 0;
-  int64_t L = 0;
-  for (int64_t r = 1; r < n_ranks; ++r) {
-    const double target = pre[nlayers] * (double)r / (double)n_ranks;
-    while (L < nlayers && pre[L + 1] <= target) ++L;
-    // pick the closer boundary of the two around the target
-    int64_t cut = L;
-    if (L < nlayers && (target - pre[L]) > (pre[L + 1] - target)) cut = L + 1;
-    cut = std::max<int64_t>(cut, ceil_div(k_bounds[r - 1], align));
-    k_bounds[r] = std::min(nz, cut * align);
+  // contiguous partition of the layers into n_ranks slabs minimising the costliest slab
+  // (exact dynamic programme; nlayers <= nz/align is small)
+  const int64_t R = n_ranks;
+  const double inf = 1e300;
+  std::vector<double> best((size_t)(R + 1) * (nlayers + 1), inf);
+  std::vector<int64_t> arg((size_t)(R + 1) * (nlayers + 1), 0);
+  auto B = [&](int64_t r, int64_t i) -> double& { return best[(size_t)r * (nlayers + 1) + i]; };
+  auto A = [&](int64_t r, int64_t i) -> int64_t& { return arg[(size_t)r * (nlayers + 1) + i]; };
+  B(0, 0) = 0.0;
+  for (int64_t r = 1; r <= R; ++r)
+    for (int64_t i = 0; i <= nlayers; ++i)
+      for (int64_t j = 0; j <= i; ++j) {  // slab r-1 = layers [j, i)
+        if (B(r - 1, j) >= inf) continue;
+        const double v = std::max(B(r - 1, j), pre[i] - pre[j]);
+        if (v < B(r, i) - 1e-12 * std::abs(v)) {
+          B(r, i) = v;
+          A(r, i) = j;
+        }
+      }
+  {
+    int64_t i = nlayers;
+    for (int64_t r = R; r >= 1; --r) {
+      k_bounds[r] = std::min(nz, i * align);
+      i = A(r, i);
+    }
+    k_bounds[0] = 0;
   }
   k_bounds[n_ranks] = nz;
   for (int64_t r = 0; r < n_ranks; ++r) {
