@@ -304,3 +304,25 @@ def test_every_tile_shape_bitwise(torch_cuda, tile_cfg):
         digest = out.stdout.split()[0]
         want = ref["cfg1_uniform11" if case == "cfg1" else "cfg2_uniform12"]["baseline"]
         assert digest == want, (case, tile_cfg, out.stdout)
+
+
+@pytest.mark.parametrize("jitter", [False, True])
+@pytest.mark.parametrize("path", ["tiled", "tiled_check"])
+def test_awkward_medium_sizes_bitwise(torch_cuda, jitter, path):
+    """Partial tiles in x, y and z (100 x 70 x 45 volume), a non-square detector whose
+    u pitch is not a multiple of 4, a volume that overhangs the detector (guarded loops,
+    skipped and never-queued (tile, angle) pairs), 97 angles; fast path (circular) and
+    general path (jittered matrices): GPU == C oracle, full volume, random start volume."""
+    from paper_2104_13248_b200 import geometry as G
+
+    geom = G.build_geometry(nx=100, ny=70, nz=45, nw=151, nh=130, np=97, d=400.0, D=700.0, pixel_pitch_u=1.1,
+                            pixel_pitch_v=0.9, voxel_size=1.3)
+    mats = G.jittered_matrices(geom, 2.0, 5) if jitter else G.u_offset(G.projection_matrices(geom), 7.0)
+    img = uniform(97, 130, 151, 21)
+    vol0 = np.random.default_rng(22).uniform(-1, 1, size=(45, 70, 100)).astype(np.float32)
+    out, stats = run_device(torch_cuda, img, mats, vol0, KernelVariant.BASELINE, Layout.NATURAL, Layout.NATURAL,
+                            FLAG_SETS[path])
+    ref = vol0.copy()
+    oracle.baseline(img, mats, ref)
+    assert out.tobytes() == ref.tobytes()
+    assert stats["smem_pairs"] > 0
