@@ -146,9 +146,23 @@ def cpu_sample_gups(spec, geom, mats, img_np, target_s: float = 12.0) -> dict:
     oracle.baseline(img_np, mats, vol, threads=threads, k_lo=k_lo)
     dt = time.perf_counter() - t0
     ups = nk * nx * ny * geom.np
-    return {"value": ups / dt / 1e9, "unit": "GUPS", "cores": threads, "kind": "port",
-            "sample": f"z-slab k=[{k_lo},{k_lo + nk}) of {nz} (full x,y, all {geom.np} angles), {dt:.1f} s, "
-                      f"C oracle (bit-exact restatement of _kernels.baseline), {threads} threads"}
+    out = {"value": ups / dt / 1e9, "unit": "GUPS", "cores": threads, "kind": "port",
+           "sample": f"z-slab k=[{k_lo},{k_lo + nk}) of {nz} (full x,y, all {geom.np} angles), {dt:.1f} s, "
+                     f"C oracle (bit-exact restatement of _kernels.baseline), {threads} threads"}
+    # context: the paper's fastest CPU rung, subline_prefetch with the largest
+    # nb <= 32 dividing np, on the full volume when it is small enough to finish in seconds
+    nb = max(b for b in range(1, 33) if geom.np % b == 0)
+    if nz % 2 == 0 and nx * ny * nz * geom.np <= 2e10:
+        img_t = np.ascontiguousarray(img_np.transpose(0, 2, 1))
+        vol_t = np.zeros((nx, ny, nz), np.float32)
+        t0 = time.perf_counter()
+        oracle.rung(5, img_t, mats, vol_t, nb, threads=threads)
+        dt = time.perf_counter() - t0
+        out["context"] = {"subline_prefetch": {"value": nx * ny * nz * geom.np / dt / 1e9, "unit": "GUPS", "nb": nb,
+                                               "sample": f"full volume, {dt:.1f} s, C restatement of "
+                                                         f"_kernels.subline_prefetch, {threads} threads; "
+                                                         f"not parity-valid (SURVEY F2), context only"}}
+    return out
 
 
 def run_reference(args, spec, geom, mats) -> None:
