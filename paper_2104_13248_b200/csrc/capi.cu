@@ -222,16 +222,21 @@ int make_plan(const PlanKey& key, const float* mats_host, cudaStream_t stream, P
   int smem_optin = 227 * 1024;
   cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, key.device);
 
-  // tile: the largest column tile that still gives >= 3 waves of CTAs
+  // tile: the largest column tile that still gives >= 3 waves of CTAs; short of that, two
+  // CTAs of 8 warps per SM as long as they cover every SM (thin multi-GPU slabs: one wave of
+  // full SMs beats a second, mostly idle wave of the small tile -- cfg1 at 8 ranks); tiny
+  // problems, whose time is per-angle latency, keep the smallest tile
   int pick = 2;
+  int64_t tiles_c[3];
+  for (int c = 0; c < 3; ++c)
+    tiles_c[c] = ceil_div(key.nx, 8 * kTiles[c].NWX) * ceil_div(key.ny, 4 * kTiles[c].NWY) * ceil_div(key.nz, kZR);
   for (int c = 0; c < 3; ++c) {
-    const int64_t tiles =
-        ceil_div(key.nx, 8 * kTiles[c].NWX) * ceil_div(key.ny, 4 * kTiles[c].NWY) * ceil_div(key.nz, kZR);
-    if (tiles >= 3LL * sms * kTiles[c].MINB) {
+    if (tiles_c[c] >= 3LL * sms * kTiles[c].MINB) {
       pick = c;
       break;
     }
   }
+  if (pick == 2 && tiles_c[1] >= sms) pick = 1;
   bool may_split = pick == 0;  // candidate for two CTAs of 8 warps per SM (cfg 1), see below
   if (const char* env = std::getenv("CBP_TILE_CFG")) {  // tuning override
     const int forced = std::atoi(env);
