@@ -9,7 +9,7 @@
  *   cbp_backproject_f32      <- conebp._kernels.baseline / transpose / share /
  *                               symmetry / subline / subline_prefetch
  *                               (pkg/src/conebp/_kernels.py:29-369), dispatched
- *                               by pkg/src/conebp/backprojector.py:199-205,528,576
+ *                               by pkg/src/conebp/backprojector.py:159,199-206
  *   cbp_backproject_host_f32 <- conebp.backproject (backprojector.py:225-238) with
  *                               host numpy buffers: copies in, computes, copies out
  *   cbp_stage_projections    <- conebp.tensors.transpose_projections (tensors.py:138-147)
@@ -20,8 +20,14 @@
  *   cbp_count_ops            <- conebp.reference.ref_baseline / ref_optimized counters
  *                               (reference.py:26-290) as exposed through count=True
  *                               (backprojector.py:153-157,193-197)
+ *   cbp_backproject_window   <- the same on a chunk of angles (band buffers that hold only
+ *                               angles [s_base, s_base+n_staged), multi-GPU pipelining)
  *   cbp_slab_plan            <- none in the reference: cost-balanced z-slab partition and
  *                               per-slab detector-row bands
+ *   cbp_backproject_multi    <- none in the reference (its parallelism is numba prange over
+ *                               z, _kernels.py:42): the single-process z-slab driver over
+ *                               several devices, bands moved by the copy engines
+ *   cbp_copy_band, cbp_ipc_* <- the band transport of the one-process-per-GPU driver
  *
  * Conventions
  *  - All sizes are int64_t element counts.  Buffers are C-contiguous float32.
@@ -70,7 +76,7 @@ extern "C" {
 /* flags */
 #define CBP_FLAG_NAIVE 1u        /* one thread per voxel, global gathers (reference-simple GPU path) */
 #define CBP_FLAG_NO_SMEM 2u      /* tiled kernel, but gather from global memory (no TMA staging) */
-#define CBP_FLAG_FMA_LERP 4u     /* reserved: contract the lerps into FMA (not bit-exact) */
+#define CBP_FLAG_FMA_LERP 4u     /* tolerance mode: the three lerps as FMAs (not bit-exact, see below) */
 #define CBP_FLAG_CHECK 8u        /* verify every shared-memory sample against the TMA box (debug) */
 
 /* Library version (major*10000 + minor*100 + patch). */
@@ -117,6 +123,19 @@ int cbp_backproject_staged(const float* staged_dev, int64_t pitch, int64_t np, i
                            int64_t ny, int64_t nz, int64_t k0, int64_t nz_total,
                            int64_t s_begin, int64_t s_end, int variant, unsigned flags,
                            void* cuda_stream);
+
+/*
+ * cbp_backproject_staged on a buffer that holds only angles [s_base, s_base + n_staged)
+ * (layout [n_staged][band_rows][pitch]); [s_begin, s_end) must lie inside that window.
+ * Matrices are still the whole stack's (np x 12).  Lets a z-slab rank back-project each
+ * angle chunk of its band from a small double buffer as soon as the chunk has landed.
+ */
+int cbp_backproject_window(const float* staged_dev, int64_t pitch, int64_t np, int64_t nh,
+                           int64_t nw, int64_t band_v0, int64_t band_rows, int64_t s_base,
+                           int64_t n_staged, const float* mats_host, float* vol_dev,
+                           int vol_layout, int64_t nx, int64_t ny, int64_t nz, int64_t k0,
+                           int64_t nz_total, int64_t s_begin, int64_t s_end, int variant,
+                           unsigned flags, void* cuda_stream);
 
 /*
  * End-to-end call on HOST buffers (pinned or pageable): copies img and vol to the
@@ -187,6 +206,46 @@ int cbp_forward_project_f32(const float* vol_dev, int64_t nx, int64_t ny, int64_
 int cbp_fdk_filter_f32(const float* raw_dev, int64_t np, int64_t nh, int64_t nw, double D,
                        double pixel_pitch_u, double pixel_pitch_v, double cu, double cv,
                        double tau, float* out_dev, int64_t pitch, void* cuda_stream);
+
+/*
+ * Single-process multi-GPU z-slab back-projection.  img_dev is the
+ * NATURAL stack [np][nh][nw] on devices[0] (the root); slab_dev[r] is the NATURAL slab
+ * [k_bounds[r+1]-k_bounds[r]][ny][nx] of rank r on devices[r] (k_bounds from
+ * cbp_slab_plan; devices may repeat, e.g. all 0 to run every rank on one GPU).  Each rank
+ * receives only its slab's detector-row band, in n_chunks angle chunks copied by the copy
+ * engines (cudaMemcpy3DPeerAsync, P2P over NVLink when peers can access each other) into a
+ * double buffer, and back-projects chunk c while chunk c+1 is in flight; rank 0 reads the
+ * root stack in place when nw % 4 == 0.  No reduction: every voxel has one writer
+ * (_kernels.py:12-14), and chunks accumulate in ascending angle order, so the slabs are
+ * bitwise identical to a single-GPU launch.  Synchronous: waits for prior work on every
+ * device, returns when all slabs are complete.  stats5 (may be NULL) as cbp_sync_status,
+ * summed over ranks; CBP_EBAND if any sample fell outside its band.
+ */
+int cbp_backproject_multi(const float* img_dev, int64_t np, int64_t nh, int64_t nw,
+                          const float* mats_host, float* const* slab_dev, int64_t nx, int64_t ny,
+                          int64_t nz, const int64_t* k_bounds, int n_gpus, const int* devices,
+                          int variant, unsigned flags, int64_t n_chunks, int64_t* stats5);
+
+/*
+ * Copy angles [s0, s1) x detector rows [v0, v0+rows) of a NATURAL stack [np][nh][nw]
+ * that lives on device src_device (-1: the current device; an IPC-mapped pointer is fine)
+ * into the staging layout [s1-s0][rows][pitch] on the current device, with the copy
+ * engines (no SM work), stream-ordered on cuda_stream.  Pad columns are not written.
+ */
+int cbp_copy_band(const float* img_dev, int src_device, int64_t np, int64_t nh, int64_t nw,
+                  int64_t s0, int64_t s1, int64_t v0, int64_t rows, float* dst_dev,
+                  int64_t pitch, void* cuda_stream);
+
+/* CUDA IPC for the one-process-per-GPU driver: export a device pointer (64-byte handle of
+ * its allocation plus the pointer's offset in it), map it in another process, unmap. */
+int cbp_ipc_export(const void* dev_ptr, void* handle64, int64_t* offset);
+int cbp_ipc_open(const void* handle64, int64_t offset, void** dev_ptr);
+int cbp_ipc_close(void* dev_ptr, int64_t offset);
+
+/* Diagnostic: count the floats with bit patterns in [lo_bits, hi_bits) whose reciprocal by
+ * the kernels' branch-free rcp_rn_normal differs from __frcp_rn (IEEE 1/z); first_bad gets
+ * the smallest mismatching pattern (0xffffffff if none). */
+int cbp_selftest_rcp(uint32_t lo_bits, uint32_t hi_bits, uint64_t* mismatches, uint32_t* first_bad);
 
 /* Release cached plans and device scratch owned by the library on this device. */
 int cbp_release(void);

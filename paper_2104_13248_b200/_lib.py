@@ -28,6 +28,7 @@ TRANSPOSED = 1
 
 FLAG_NAIVE = 1
 FLAG_NO_SMEM = 2
+FLAG_FMA_LERP = 4
 FLAG_CHECK = 8
 
 _f32p = POINTER(c_float)
@@ -80,6 +81,24 @@ SIGNATURES = {
         [c_void_p, c_int64, c_int64, c_int64, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
          ctypes.c_double, ctypes.c_double, c_void_p, c_int64, c_void_p],
     ),
+    "cbp_backproject_window": (
+        c_int,
+        [c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, _f32p, c_void_p, c_int,
+         c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_int, c_uint, c_void_p],
+    ),
+    "cbp_backproject_multi": (
+        c_int,
+        [c_void_p, c_int64, c_int64, c_int64, _f32p, POINTER(c_void_p), c_int64, c_int64, c_int64, _i64p, c_int,
+         POINTER(c_int), c_int, c_uint, c_int64, _i64p],
+    ),
+    "cbp_copy_band": (
+        c_int,
+        [c_void_p, c_int, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p, c_int64, c_void_p],
+    ),
+    "cbp_ipc_export": (c_int, [c_void_p, c_void_p, _i64p]),
+    "cbp_ipc_open": (c_int, [c_void_p, c_int64, POINTER(c_void_p)]),
+    "cbp_ipc_close": (c_int, [c_void_p, c_int64]),
+    "cbp_selftest_rcp": (c_int, [ctypes.c_uint32, ctypes.c_uint32, POINTER(ctypes.c_uint64), POINTER(ctypes.c_uint32)]),
     "cbp_release": (c_int, []),
     "cbp_last_plan": (c_int, [_i64p]),
 }

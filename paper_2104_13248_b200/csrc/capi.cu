@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -59,13 +60,20 @@ EncodeTiledFn get_encode() {
 }
 
 // ---------------------------------------------------------------- helpers
-uint64_t fnv1a(const void* data, size_t n, uint64_t h = 1469598103934665603ull) {
+// 64-bit FNV-1a over 8-byte words (the matrices are hashed on every launch: a word at a
+// time is 8x cheaper than bytes; cfg4's 96 KiB of matrices hash in ~10 us)
+uint64_t hash_words(const void* data, size_t n) {
+  uint64_t h = 1469598103934665603ull;
   const unsigned char* b = static_cast<const unsigned char*>(data);
-  for (size_t i = 0; i < n; ++i) {
-    h ^= b[i];
-    h *= 1099511628211ull;
+  size_t i = 0;
+  for (; i + 8 <= n; i += 8) {
+    uint64_t w;
+    std::memcpy(&w, b + i, 8);
+    h = (h ^ w) * 1099511628211ull;
+    h ^= h >> 29;
   }
-  return h;
+  for (; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+  return h ^ (uint64_t)n;
 }
 
 bool mats_finite(const float* m, int64_t n) {
@@ -83,12 +91,36 @@ bool fast_path_ok(const float* mats, int64_t np, int variant) {
   return true;
 }
 
+// A device allocation shared by cached plans and the launches that read it.  It is freed
+// when the last reference goes (a plan evicted while another thread is still launching
+// with it keeps it alive); before the free the owning device is drained, since launches
+// queued on any stream may still read it.
+struct DevBuf {
+  void* p = nullptr;
+  int dev = -1;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (!p) return;
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && cudaSetDevice(dev) == cudaSuccess) {
+      cudaDeviceSynchronize();
+      cudaFree(p);
+      cudaSetDevice(cur);
+    }
+    cudaGetLastError();
+  }
+};
+
 struct Plan {
   int cfg = 0, TX = 32, TY = 16, NW = 16, wb = 0, hb = 0, stages = 0;
   int kind = 1;  // 0 naive, 1 tiled fast, 2 tiled general
   size_t smem = 0;
-  float* mats_dev = nullptr;
+  std::shared_ptr<DevBuf> mats;  // np x 12 float32 on the plan's device
+  const float* mats_dev() const { return static_cast<const float*>(mats->p); }
   int device = -1;
+  uint64_t last_use = 0;
 };
 
 struct PlanKey {
@@ -100,12 +132,19 @@ struct PlanKey {
   }
 };
 
-std::mutex g_mu;
+std::mutex g_mu;  // guards g_plans, g_stats, g_smem_set, g_use_clock
 std::map<PlanKey, Plan> g_plans;
-std::map<int, unsigned long long*> g_stats;  // per-device status counters [8]
+std::map<std::pair<int, uintptr_t>, unsigned long long*> g_stats;  // status counters [8] per (device, stream)
+std::map<std::pair<int, const void*>, size_t> g_smem_set;          // dynamic smem attribute set per kernel
+uint64_t g_use_clock = 0;
+constexpr int kPlansPerDevice = 16;
 
-int get_stats(int dev, unsigned long long** out) {
-  auto it = g_stats.find(dev);
+// status counters of (device, stream): every launch on a stream accumulates into its
+// own buffer, so cbp_sync_status on one stream never reads or clears another's
+int get_stats(int dev, cudaStream_t st, unsigned long long** out) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  const auto key = std::make_pair(dev, reinterpret_cast<uintptr_t>(st));
+  auto it = g_stats.find(key);
   if (it != g_stats.end()) {
     *out = it->second;
     return CBP_OK;
@@ -113,7 +152,7 @@ int get_stats(int dev, unsigned long long** out) {
   unsigned long long* p = nullptr;
   CK(cudaMalloc(&p, 8 * sizeof(unsigned long long)), "cudaMalloc(stats)");
   CK(cudaMemset(p, 0, 8 * sizeof(unsigned long long)), "cudaMemset(stats)");
-  g_stats[dev] = p;
+  g_stats[key] = p;
   *out = p;
   return CBP_OK;
 }
@@ -208,8 +247,11 @@ int make_plan(const PlanKey& key, const float* mats_host, cudaStream_t stream, P
   plan = Plan();
   plan.device = key.device;
   const int64_t n12 = key.np * 12;
-  CK(cudaMalloc(&plan.mats_dev, n12 * sizeof(float)), "cudaMalloc(mats)");
-  CK(cudaMemcpyAsync(plan.mats_dev, mats_host, n12 * sizeof(float), cudaMemcpyHostToDevice, stream), "upload mats");
+  plan.mats = std::make_shared<DevBuf>();
+  plan.mats->dev = key.device;
+  CK(cudaMalloc(&plan.mats->p, n12 * sizeof(float)), "cudaMalloc(mats)");
+  // synchronous: mats_host is only borrowed for the duration of the call
+  CK(cudaMemcpy(plan.mats->p, mats_host, n12 * sizeof(float), cudaMemcpyHostToDevice), "upload mats");
   if (key.kind_req == 0) {
     plan.kind = 0;
     return CBP_OK;
@@ -264,7 +306,7 @@ int make_plan(const PlanKey& key, const float* mats_host, cudaStream_t stream, P
   const int64_t pairs = n_tiles * ceil_div(key.np, astride);
   const int wpb = 8;
   dim3 g((unsigned)ceil_div(pairs, wpb)), b(32 * wpb);
-  int rc = run_footprint(key.variant, g, b, stream, plan.mats_dev, (int)key.np, (int)key.nw, (int)key.nh, (int)key.nx,
+  int rc = run_footprint(key.variant, g, b, stream, plan.mats_dev(), (int)key.np, (int)key.nw, (int)key.nh, (int)key.nx,
                          (int)key.ny, (int)key.nz, (int)key.k0, (int)key.nz_total, plan.TX, plan.TY, tx, ty, tz,
                          astride, hist, hist + nbins, nbins, (int)key.band_v0);
   if (rc) return rc;
@@ -281,11 +323,7 @@ int make_plan(const PlanKey& key, const float* mats_host, cudaStream_t stream, P
     uint64_t sampled = 0;
     for (int i = 0; i < nbins; ++i) sampled += h[i];
     const double missed = 1.0 - (double)sampled / (double)std::max<int64_t>(1, pairs);
-    if (missed < 0.25) {
-      cudaFree(plan.mats_dev);
-      plan.mats_dev = nullptr;
-      return make_plan(key, mats_host, stream, plan, 1);
-    }
+    if (missed < 0.25) return make_plan(key, mats_host, stream, plan, 1);
   }
 
   auto quantile = [&](const unsigned* hh, double q) {
@@ -327,37 +365,75 @@ int make_plan(const PlanKey& key, const float* mats_host, cudaStream_t stream, P
   return CBP_OK;
 }
 
-int get_plan(const PlanKey& key, const float* mats_host, cudaStream_t stream, Plan** out) {
-  std::lock_guard<std::mutex> lk(g_mu);
-  auto it = g_plans.find(key);
-  if (it != g_plans.end()) {
-    *out = &it->second;
-    return CBP_OK;
-  }
-  if (g_plans.size() >= 16) {  // simple bound: drop everything on this device
-    for (auto& kv : g_plans)
-      if (kv.second.mats_dev) cudaFree(kv.second.mats_dev);
-    g_plans.clear();
+// Plan for `key`, returned BY VALUE (its matrices are reference counted): callers use it
+// after the lock is gone, while other threads may evict it.  Plans are built outside the
+// lock; eviction is per device, least recently used first.
+int get_plan(const PlanKey& key, const float* mats_host, cudaStream_t stream, Plan* out) {
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_plans.find(key);
+    if (it != g_plans.end()) {
+      it->second.last_use = ++g_use_clock;
+      *out = it->second;
+      return CBP_OK;
+    }
   }
   Plan p;
   int rc = make_plan(key, mats_host, stream, p);
-  if (rc) {
-    if (p.mats_dev) cudaFree(p.mats_dev);
-    return rc;
+  if (rc) return rc;
+  std::shared_ptr<DevBuf> evicted;  // released after the lock: its destructor drains the device
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_plans.find(key);
+    if (it != g_plans.end()) {  // another thread built the same plan meanwhile
+      it->second.last_use = ++g_use_clock;
+      *out = it->second;
+      return CBP_OK;
+    }
+    int on_dev = 0;
+    auto lru = g_plans.end();
+    for (auto i = g_plans.begin(); i != g_plans.end(); ++i) {
+      if (i->first.device != key.device) continue;
+      ++on_dev;
+      if (lru == g_plans.end() || i->second.last_use < lru->second.last_use) lru = i;
+    }
+    if (on_dev >= kPlansPerDevice && lru != g_plans.end()) {
+      evicted = lru->second.mats;
+      g_plans.erase(lru);
+    }
+    p.last_use = ++g_use_clock;
+    g_plans.emplace(key, p);
   }
-  auto res = g_plans.emplace(key, p);
-  *out = &res.first->second;
+  *out = p;
   return CBP_OK;
 }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel) and size
+int ensure_smem(int dev, const void* fn, size_t smem) {
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_smem_set.find({dev, fn});
+    if (it != g_smem_set.end() && it->second >= smem) return CBP_OK;
+  }
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "set smem attribute");
+  std::lock_guard<std::mutex> lk(g_mu);
+  size_t& v = g_smem_set[{dev, fn}];
+  v = std::max(v, smem);
+  return CBP_OK;
+}
+
+// Dimensions the float32 index arithmetic supports.  A detector narrower or shorter than
+// two pixels is legal (the reference accepts any size >= 1, tensors.py:44-58) and samples
+// nothing: the guard x < nw-1 / y < nh-1 (_kernels.py:52) never passes, so the entry
+// points return without launching.
 int check_dims(int64_t np, int64_t nh, int64_t nw, int64_t nx, int64_t ny, int64_t nz) {
-  if (np < 1 || nh < 2 || nw < 2 || nx < 1 || ny < 1 || nz < 1)
-    return fail(CBP_EINVAL, "dimensions must be >= 1 (detector >= 2x2)");
+  if (np < 1 || nh < 1 || nw < 1 || nx < 1 || ny < 1 || nz < 1) return fail(CBP_EINVAL, "dimensions must be >= 1");
   if (nh >= (1 << 23) || nw >= (1 << 23) || np >= (1 << 30) || nx >= (1 << 24) || ny >= (1 << 24) ||
       nz >= (1 << 24))
     return fail(CBP_EINVAL, "dimension too large for float32 index arithmetic");
   return CBP_OK;
 }
+bool samples_nothing(int64_t nh, int64_t nw) { return nh < 2 || nw < 2; }
 
 // keep freed stream-ordered allocations cached in the device's default pool (the
 // host path allocates projection-sized buffers on every call)
@@ -395,12 +471,168 @@ void vol_strides(int layout, int64_t nx, int64_t ny, int64_t nz, long long& sx, 
   }
 }
 
+// One back-projection launch on staged projections (every public kernel entry point
+// ends here).  `staged` holds detector rows [band_v0, band_v0 + band_rows) of angles
+// [s_base, s_base + n_staged) in the layout [n_staged][band_rows][pitch]; the launch
+// accumulates angles [s_begin, s_end) into slab [k0, k0 + nz) of a volume of nz_total
+// slices; device-side status counters go to `stats`.
+struct StagedCall {
+  const float* staged;
+  int64_t pitch, np, nh, nw, band_v0, band_rows;
+  const float* mats_host;
+  float* vol;
+  int vol_layout;
+  int64_t nx, ny, nz, k0, nz_total, s_begin, s_end, s_base, n_staged;
+  int variant;
+  unsigned flags;
+};
+
+int validate_staged(StagedCall& c) {
+  int rc = check_dims(c.np, c.nh, c.nw, c.nx, c.ny, c.nz);
+  if (rc) return rc;
+  if (!c.staged || !c.mats_host || !c.vol) return fail(CBP_EINVAL, "null buffer");
+  if (c.variant < 0 || c.variant > 5) return fail(CBP_EINVAL, "unknown kernel variant");
+  if (c.vol_layout != CBP_NATURAL && c.vol_layout != CBP_TRANSPOSED) return fail(CBP_EINVAL, "unknown volume layout");
+  if (c.k0 < 0 || c.nz_total < c.k0 + c.nz) return fail(CBP_EINVAL, "slab [k0, k0+nz) outside nz_total");
+  if (v_mirror(c.variant) && (c.nz_total & 1)) return fail(CBP_EINVAL, "symmetry kernels need an even nz");
+  if (c.s_end <= 0) c.s_end = c.np;
+  if (c.s_begin < 0 || c.s_begin > c.s_end || c.s_end > c.np) return fail(CBP_EINVAL, "invalid angle range");
+  if (c.n_staged <= 0) c.n_staged = c.np - c.s_base;
+  if (c.s_base < 0 || c.s_base > c.s_begin || c.s_base + c.n_staged < c.s_end || c.s_base + c.n_staged > c.np)
+    return fail(CBP_EINVAL, "staged angle window does not cover [s_begin, s_end)");
+  if (!mats_finite(c.mats_host, c.np * 12)) return fail(CBP_EINVAL, "projection matrices contain non-finite values");
+  if (samples_nothing(c.nh, c.nw)) return CBP_OK;
+  if (c.band_v0 < 0 || c.band_rows < 2 || c.band_v0 + c.band_rows > c.nh || c.pitch < c.nw || (c.pitch & 3))
+    return fail(CBP_EINVAL, "invalid detector-row band or pitch");
+  return CBP_OK;
+}
+
+int launch_staged(StagedCall c, unsigned long long* stats, cudaStream_t st) {
+  int rc = validate_staged(c);
+  if (rc) return rc;
+  if (c.s_begin == c.s_end || samples_nothing(c.nh, c.nw)) return CBP_OK;
+  int dev;
+  rc = current_device(&dev);
+  if (rc) return rc;
+
+  PlanKey key;
+  std::memset(&key, 0, sizeof(key));
+  key.device = dev;
+  key.variant = (c.variant == V_PREFETCH) ? V_SUBLINE : c.variant;
+  key.kind_req = (c.flags & CBP_FLAG_NAIVE) ? 0 : 1;
+  key.np = c.np; key.nh = c.nh; key.nw = c.nw; key.band_v0 = c.band_v0; key.band_rows = c.band_rows;
+  key.nx = c.nx; key.ny = c.ny; key.nz = c.nz; key.k0 = c.k0; key.nz_total = c.nz_total;
+  key.mhash = hash_words(c.mats_host, (size_t)c.np * 12 * sizeof(float));
+  Plan plan;
+  rc = get_plan(key, c.mats_host, st, &plan);
+  if (rc) return rc;
+
+  BPParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.proj = c.staged;
+  p.mats = plan.mats_dev();
+  p.vol = c.vol;
+  vol_strides(c.vol_layout, c.nx, c.ny, c.nz, p.vsx, p.vsy, p.vsz);
+  p.np = (int)c.np; p.nw = (int)c.nw; p.nh = (int)c.nh; p.pitch = (int)c.pitch;
+  p.band_v0 = (int)c.band_v0; p.band_rows = (int)c.band_rows;
+  p.nx = (int)c.nx; p.ny = (int)c.ny; p.nz = (int)c.nz; p.k0 = (int)c.k0; p.nz_total = (int)c.nz_total;
+  p.s_begin = (int)c.s_begin; p.s_end = (int)c.s_end; p.s_base = (int)c.s_base;
+  p.stats = stats;
+
+  if (plan.kind == 0) {
+    const int64_t nvox = c.nx * c.ny * c.nz;
+    dim3 b(256), g((unsigned)ceil_div(nvox, 256));
+    void* args[] = {&p};
+    CK(cudaLaunchKernel(naive_kernel_ptr(key.variant), g, b, args, 0, st), "naive kernel launch");
+    int64_t lp[9] = {1, 1, 1, 0, 0, 0, (int64_t)g.x, 0, 0};
+    std::memcpy(g_last_plan, lp, sizeof(lp));
+    return CBP_OK;
+  }
+
+  // tiled TMA path
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(CBP_ECUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+  p.tiles_x = (int)ceil_div(c.nx, plan.TX);
+  p.tiles_y = (int)ceil_div(c.ny, plan.TY);
+  p.tiles_z = (int)ceil_div(c.nz, kZR);
+  p.wb = plan.wb;
+  p.hb = plan.hb;
+  p.stages = plan.stages;
+  if (c.flags & CBP_FLAG_NO_SMEM) p.hb = 1;  // every pair through the global path: make the box unusable
+  CUtensorMap tmap;
+  std::memset(&tmap, 0, sizeof(tmap));
+  cuuint64_t gdim[3] = {(cuuint64_t)c.nw, (cuuint64_t)c.band_rows, (cuuint64_t)c.n_staged};
+  cuuint64_t gstride[2] = {(cuuint64_t)c.pitch * 4, (cuuint64_t)(c.pitch * c.band_rows) * 4};
+  cuuint32_t box[3] = {(cuuint32_t)plan.wb, (cuuint32_t)plan.hb, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult cr = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(c.staged), gdim, gstride, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) {
+    char buf[160];
+    std::snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled failed (%d): box %dx%d pitch %lld", (int)cr, plan.wb,
+                  plan.hb, (long long)c.pitch);
+    return fail(CBP_ECUDA, buf);
+  }
+  const void* fn = tiled_kernel_ptr(key.variant, plan.kind == 2, plan.cfg, (c.flags & CBP_FLAG_CHECK) != 0);
+  rc = ensure_smem(dev, fn, plan.smem);
+  if (rc) return rc;
+  const int64_t blocks = (int64_t)p.tiles_x * p.tiles_y * p.tiles_z;
+  if (blocks > 0x7fffffffLL) return fail(CBP_EINVAL, "volume too large for one launch");
+  if (kTilePool[plan.cfg] != 0) {  // setmaxnreg.inc would wait forever on a smaller pool
+    cudaFuncAttributes fa{};
+    CK(cudaFuncGetAttributes(&fa, fn), "cudaFuncGetAttributes(tiled kernel)");
+    if (fa.numRegs != kTilePool[plan.cfg]) {
+      char buf[128];
+      std::snprintf(buf, sizeof buf, "tiled kernel register pool %d != %d assumed by its setmaxnreg split",
+                    fa.numRegs, kTilePool[plan.cfg]);
+      return fail(CBP_ECUDA, buf);
+    }
+  }
+  dim3 g((unsigned)blocks), b(kTileThreads[plan.cfg]);
+  void* args[] = {&tmap, &p};
+  CK(cudaLaunchKernel(fn, g, b, args, plan.smem, st), "tiled kernel launch");
+  int64_t lp[9] = {plan.TX, plan.TY, kZR, plan.wb, plan.hb, plan.stages, blocks, (int64_t)plan.smem, plan.kind};
+  std::memcpy(g_last_plan, lp, sizeof(lp));
+  return CBP_OK;
+}
+
+// read (and clear) a status buffer on `st`; CBP_EBAND when samples fell outside a band
+int read_stats(unsigned long long* d, cudaStream_t st, int64_t* stats5) {
+  unsigned long long h[8] = {0};
+  CK(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, st), "read status");
+  CK(cudaMemsetAsync(d, 0, sizeof(h), st), "reset status");
+  CK(cudaStreamSynchronize(st), "status sync");
+  if (stats5)
+    for (int q = 0; q < 5; ++q) stats5[q] += (int64_t)h[q];
+  if (h[3]) {
+    char buf[128];
+    std::snprintf(buf, sizeof buf, "%llu samples fell outside the slab's detector-row band", h[3]);
+    return fail(CBP_EBAND, buf);
+  }
+  return CBP_OK;
+}
+
+// private status buffer for calls that synchronise before returning (host path, multi-GPU)
+struct ScopedStats {
+  unsigned long long* d = nullptr;
+  int alloc(cudaStream_t st) {
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&d), 8 * sizeof(unsigned long long), st), "alloc status");
+    CK(cudaMemsetAsync(d, 0, 8 * sizeof(unsigned long long), st), "clear status");
+    return CBP_OK;
+  }
+  void release(cudaStream_t st) {
+    if (d) cudaFreeAsync(d, st);
+    d = nullptr;
+  }
+};
+
 }  // namespace
 
 // =================================================================== C ABI
 extern "C" {
 
-int cbp_version(void) { return 100; }  // 0.1.0
+int cbp_version(void) { return 200; }  // 0.2.0
 
 const char* cbp_last_error(void) { return g_err.c_str(); }
 
@@ -435,115 +667,31 @@ int cbp_stage_projections(const float* img_dev, int img_layout, int64_t np, int6
   return CBP_OK;
 }
 
+int cbp_backproject_window(const float* staged_dev, int64_t pitch, int64_t np, int64_t nh, int64_t nw,
+                           int64_t band_v0, int64_t band_rows, int64_t s_base, int64_t n_staged,
+                           const float* mats_host, float* vol_dev, int vol_layout, int64_t nx, int64_t ny, int64_t nz,
+                           int64_t k0, int64_t nz_total, int64_t s_begin, int64_t s_end, int variant, unsigned flags,
+                           void* cuda_stream) {
+  StagedCall c{staged_dev, pitch,    np, nh, nw, band_v0, band_rows, mats_host, vol_dev, vol_layout, nx, ny, nz, k0,
+               nz_total,   s_begin, s_end, s_base, n_staged, variant, flags};
+  int dev;
+  int rc = validate_staged(c);
+  if (rc || c.s_begin == c.s_end || samples_nothing(nh, nw)) return rc;
+  rc = current_device(&dev);
+  if (rc) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  unsigned long long* stats = nullptr;
+  rc = get_stats(dev, st, &stats);
+  if (rc) return rc;
+  return launch_staged(c, stats, st);
+}
+
 int cbp_backproject_staged(const float* staged_dev, int64_t pitch, int64_t np, int64_t nh, int64_t nw,
                            int64_t band_v0, int64_t band_rows, const float* mats_host, float* vol_dev, int vol_layout,
                            int64_t nx, int64_t ny, int64_t nz, int64_t k0, int64_t nz_total, int64_t s_begin,
                            int64_t s_end, int variant, unsigned flags, void* cuda_stream) {
-  int rc = check_dims(np, nh, nw, nx, ny, nz);
-  if (rc) return rc;
-  if (!staged_dev || !mats_host || !vol_dev) return fail(CBP_EINVAL, "null buffer");
-  if (variant < 0 || variant > 5) return fail(CBP_EINVAL, "unknown kernel variant");
-  if (vol_layout != CBP_NATURAL && vol_layout != CBP_TRANSPOSED) return fail(CBP_EINVAL, "unknown volume layout");
-  if (band_v0 < 0 || band_rows < 2 || band_v0 + band_rows > nh || pitch < nw || (pitch & 3))
-    return fail(CBP_EINVAL, "invalid detector-row band or pitch");
-  if (k0 < 0 || nz_total < k0 + nz) return fail(CBP_EINVAL, "slab [k0, k0+nz) outside nz_total");
-  if (v_mirror(variant) && (nz_total & 1)) return fail(CBP_EINVAL, "symmetry kernels need an even nz");
-  if (s_end <= 0) s_end = np;
-  if (s_begin < 0 || s_begin > s_end || s_end > np) return fail(CBP_EINVAL, "invalid angle range");
-  if (!mats_finite(mats_host, np * 12)) return fail(CBP_EINVAL, "projection matrices contain non-finite values");
-  if (s_begin == s_end) return CBP_OK;
-  int dev;
-  rc = current_device(&dev);
-  if (rc) return rc;
-  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
-
-  PlanKey key;
-  std::memset(&key, 0, sizeof(key));
-  key.device = dev;
-  key.variant = (variant == V_PREFETCH) ? V_SUBLINE : variant;
-  key.kind_req = (flags & CBP_FLAG_NAIVE) ? 0 : 1;
-  key.np = np; key.nh = nh; key.nw = nw; key.band_v0 = band_v0; key.band_rows = band_rows;
-  key.nx = nx; key.ny = ny; key.nz = nz; key.k0 = k0; key.nz_total = nz_total;
-  key.mhash = fnv1a(mats_host, (size_t)np * 12 * sizeof(float));
-  Plan* plan = nullptr;
-  rc = get_plan(key, mats_host, st, &plan);
-  if (rc) return rc;
-  unsigned long long* stats = nullptr;
-  {
-    std::lock_guard<std::mutex> lk(g_mu);
-    rc = get_stats(dev, &stats);
-  }
-  if (rc) return rc;
-
-  BPParams p;
-  std::memset(&p, 0, sizeof(p));
-  p.proj = staged_dev;
-  p.mats = plan->mats_dev;
-  p.vol = vol_dev;
-  vol_strides(vol_layout, nx, ny, nz, p.vsx, p.vsy, p.vsz);
-  p.np = (int)np; p.nw = (int)nw; p.nh = (int)nh; p.pitch = (int)pitch;
-  p.band_v0 = (int)band_v0; p.band_rows = (int)band_rows;
-  p.nx = (int)nx; p.ny = (int)ny; p.nz = (int)nz; p.k0 = (int)k0; p.nz_total = (int)nz_total;
-  p.s_begin = (int)s_begin; p.s_end = (int)s_end;
-  p.stats = stats;
-
-  if (plan->kind == 0) {
-    const int64_t nvox = nx * ny * nz;
-    dim3 b(256), g((unsigned)ceil_div(nvox, 256));
-    void* args[] = {&p};
-    CK(cudaLaunchKernel(naive_kernel_ptr(key.variant), g, b, args, 0, st), "naive kernel launch");
-    int64_t lp[9] = {1, 1, 1, 0, 0, 0, (int64_t)g.x, 0, 0};
-    std::memcpy(g_last_plan, lp, sizeof(lp));
-    return CBP_OK;
-  }
-
-  // tiled TMA path
-  EncodeTiledFn enc = get_encode();
-  if (!enc) return fail(CBP_ECUDA, "cuTensorMapEncodeTiled unavailable from the driver");
-  p.tiles_x = (int)ceil_div(nx, plan->TX);
-  p.tiles_y = (int)ceil_div(ny, plan->TY);
-  p.tiles_z = (int)ceil_div(nz, kZR);
-  p.wb = plan->wb;
-  p.hb = plan->hb;
-  p.stages = plan->stages;
-  if (flags & CBP_FLAG_NO_SMEM) {  // every pair through the global path: make the box unusable
-    p.hb = 1;
-  }
-  CUtensorMap tmap;
-  std::memset(&tmap, 0, sizeof(tmap));
-  cuuint64_t gdim[3] = {(cuuint64_t)nw, (cuuint64_t)band_rows, (cuuint64_t)np};
-  cuuint64_t gstride[2] = {(cuuint64_t)pitch * 4, (cuuint64_t)(pitch * band_rows) * 4};
-  cuuint32_t box[3] = {(cuuint32_t)plan->wb, (cuuint32_t)plan->hb, 1};
-  cuuint32_t estr[3] = {1, 1, 1};
-  CUresult cr = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(staged_dev), gdim, gstride, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (cr != CUDA_SUCCESS) {
-    char buf[160];
-    std::snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled failed (%d): box %dx%d pitch %lld", (int)cr, plan->wb,
-                  plan->hb, (long long)pitch);
-    return fail(CBP_ECUDA, buf);
-  }
-  const void* fn = tiled_kernel_ptr(key.variant, plan->kind == 2, plan->cfg, (flags & CBP_FLAG_CHECK) != 0);
-  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan->smem), "set smem attribute");
-  const int64_t blocks = (int64_t)p.tiles_x * p.tiles_y * p.tiles_z;
-  if (blocks > 0x7fffffffLL) return fail(CBP_EINVAL, "volume too large for one launch");
-  if (kTilePool[plan->cfg] != 0) {  // setmaxnreg.inc would wait forever on a smaller pool
-    cudaFuncAttributes fa{};
-    CK(cudaFuncGetAttributes(&fa, fn), "cudaFuncGetAttributes(tiled kernel)");
-    if (fa.numRegs != kTilePool[plan->cfg]) {
-      char buf[128];
-      std::snprintf(buf, sizeof buf, "tiled kernel register pool %d != %d assumed by its setmaxnreg split",
-                    fa.numRegs, kTilePool[plan->cfg]);
-      return fail(CBP_ECUDA, buf);
-    }
-  }
-  dim3 g((unsigned)blocks), b(kTileThreads[plan->cfg]);
-  void* args[] = {&tmap, &p};
-  CK(cudaLaunchKernel(fn, g, b, args, plan->smem, st), "tiled kernel launch");
-  int64_t lp[9] = {plan->TX, plan->TY, kZR, plan->wb, plan->hb, plan->stages, blocks, (int64_t)plan->smem, plan->kind};
-  std::memcpy(g_last_plan, lp, sizeof(lp));
-  return CBP_OK;
+  return cbp_backproject_window(staged_dev, pitch, np, nh, nw, band_v0, band_rows, 0, np, mats_host, vol_dev,
+                                vol_layout, nx, ny, nz, k0, nz_total, s_begin, s_end, variant, flags, cuda_stream);
 }
 
 int cbp_backproject_f32(const float* img_dev, int64_t np, int64_t nh, int64_t nw, int img_layout,
@@ -552,10 +700,12 @@ int cbp_backproject_f32(const float* img_dev, int64_t np, int64_t nh, int64_t nw
   int rc = check_dims(np, nh, nw, nx, ny, nz);
   if (rc) return rc;
   if (!img_dev) return fail(CBP_EINVAL, "null projection buffer");
+  if (img_layout != CBP_NATURAL && img_layout != CBP_TRANSPOSED) return fail(CBP_EINVAL, "unknown projection layout");
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
-  if (img_layout == CBP_NATURAL && (nw & 3) == 0) {  // already in the staging layout: zero copy
-    return cbp_backproject_staged(img_dev, nw, np, nh, nw, 0, nh, mats_host, vol_dev, vol_layout, nx, ny, nz, 0, nz, 0,
-                                  np, variant, flags, cuda_stream);
+  if (samples_nothing(nh, nw) || (img_layout == CBP_NATURAL && (nw & 3) == 0)) {
+    // already in the staging layout: zero copy (or nothing to sample)
+    return cbp_backproject_staged(img_dev, samples_nothing(nh, nw) ? 4 : nw, np, nh, nw, 0, nh, mats_host, vol_dev,
+                                  vol_layout, nx, ny, nz, 0, nz, 0, np, variant, flags, cuda_stream);
   }
   const int64_t pitch = cbp_staged_pitch(nw);
   float* staged = nullptr;
@@ -575,6 +725,11 @@ int cbp_backproject_host_f32(const float* img_host, int64_t np, int64_t nh, int6
   if (rc) return rc;
   if (!img_host || !vol_host || !mats_host) return fail(CBP_EINVAL, "null buffer");
   if (img_layout != CBP_NATURAL && img_layout != CBP_TRANSPOSED) return fail(CBP_EINVAL, "unknown projection layout");
+  if (vol_layout != CBP_NATURAL && vol_layout != CBP_TRANSPOSED) return fail(CBP_EINVAL, "unknown volume layout");
+  if (variant < 0 || variant > 5) return fail(CBP_EINVAL, "unknown kernel variant");
+  if (v_mirror(variant) && (nz & 1)) return fail(CBP_EINVAL, "symmetry kernels need an even nz");
+  if (!mats_finite(mats_host, np * 12)) return fail(CBP_EINVAL, "projection matrices contain non-finite values");
+  if (samples_nothing(nh, nw)) return CBP_OK;  // the volume is left unchanged, as by the reference
   int dev;
   rc = current_device(&dev);
   if (rc) return rc;
@@ -597,6 +752,7 @@ int cbp_backproject_host_f32(const float* img_host, int64_t np, int64_t nh, int6
   n_chunks = std::min<int64_t>(n_chunks, 24);
   if (const char* env = std::getenv("CBP_HOST_CHUNKS")) n_chunks = std::max<int64_t>(1, std::min<int64_t>(np, std::atoi(env)));
   keep_pool_warm(dev);
+  ScopedStats stats;
   std::vector<cudaEvent_t> ev((size_t)n_chunks, nullptr);
   e = cudaMallocAsync(reinterpret_cast<void**>(&img), ib, sk);
   if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&vol), vb, sk);
@@ -606,6 +762,7 @@ int cbp_backproject_host_f32(const float* img_host, int64_t np, int64_t nh, int6
   if (e == cudaSuccess) e = cudaMemcpyAsync(vol, vol_host, vb, cudaMemcpyHostToDevice, sk);
   if (e == cudaSuccess) e = cudaStreamSynchronize(sk);  // allocations visible to the copy stream
   if (e != cudaSuccess) rc = cuda_fail(e, "host path: allocation / volume upload");
+  if (rc == CBP_OK) rc = stats.alloc(sk);
   for (int64_t q = 0; q < n_chunks && rc == CBP_OK; ++q) {
     const int64_t s0 = np * q / n_chunks, s1 = np * (q + 1) / n_chunks;
     e = cudaMemcpyAsync(img + s0 * per_proj, img_host + s0 * per_proj, (size_t)(s1 - s0) * per_proj * 4,
@@ -616,22 +773,22 @@ int cbp_backproject_host_f32(const float* img_host, int64_t np, int64_t nh, int6
       rc = cuda_fail(e, "host path: projection upload");
       break;
     }
-    if (direct) {
-      rc = cbp_backproject_staged(img, nw, np, nh, nw, 0, nh, mats_host, vol, vol_layout, nx, ny, nz, 0, nz, s0, s1,
-                                  variant, flags, sk);
-    } else {
+    StagedCall c{img, nw, np, nh, nw, 0, nh, mats_host, vol, vol_layout, nx, ny, nz, 0, nz, s0, s1, 0, np, variant, flags};
+    if (!direct) {
       rc = cbp_stage_projections(img + s0 * per_proj, img_layout, s1 - s0, nh, nw, 0, nh, staged + s0 * nh * pitch,
                                  pitch, sk);
-      if (rc == CBP_OK)
-        rc = cbp_backproject_staged(staged, pitch, np, nh, nw, 0, nh, mats_host, vol, vol_layout, nx, ny, nz, 0, nz,
-                                    s0, s1, variant, flags, sk);
+      c.staged = staged;
+      c.pitch = pitch;
     }
+    if (rc == CBP_OK) rc = launch_staged(c, stats.d, sk);
   }
   if (rc == CBP_OK) {
     e = cudaMemcpyAsync(vol_host, vol, vb, cudaMemcpyDeviceToHost, sk);
     if (e != cudaSuccess) rc = cuda_fail(e, "host path: copy out");
   }
+  if (rc == CBP_OK) rc = read_stats(stats.d, sk, nullptr);
   cudaStreamSynchronize(sc);
+  stats.release(sk);
   if (img) cudaFreeAsync(img, sk);
   if (vol) cudaFreeAsync(vol, sk);
   if (staged) cudaFreeAsync(staged, sk);
@@ -641,7 +798,6 @@ int cbp_backproject_host_f32(const float* img_host, int64_t np, int64_t nh, int6
     if (x) cudaEventDestroy(x);
   cudaStreamDestroy(sc);
   cudaStreamDestroy(sk);
-  if (rc == CBP_OK) rc = cbp_sync_status(nullptr, nullptr);
   return rc;
 }
 
@@ -649,24 +805,35 @@ int cbp_sync_status(void* cuda_stream, int64_t* stats5) {
   int dev;
   int rc = current_device(&dev);
   if (rc) return rc;
-  unsigned long long* d = nullptr;
-  {
-    std::lock_guard<std::mutex> lk(g_mu);
-    rc = get_stats(dev, &d);
-  }
-  if (rc) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
-  unsigned long long h[8] = {0};
-  CK(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, st), "read status");
-  CK(cudaMemsetAsync(d, 0, sizeof(h), st), "reset status");
-  CK(cudaStreamSynchronize(st), "status sync");
+  unsigned long long* d = nullptr;
+  rc = get_stats(dev, st, &d);
+  if (rc) return rc;
   if (stats5)
-    for (int q = 0; q < 5; ++q) stats5[q] = (int64_t)h[q];
-  if (h[3]) {
-    char buf[128];
-    std::snprintf(buf, sizeof buf, "%llu samples fell outside the slab's detector-row band", h[3]);
-    return fail(CBP_EBAND, buf);
+    for (int q = 0; q < 5; ++q) stats5[q] = 0;
+  return read_stats(d, st, stats5);
+}
+
+int cbp_selftest_rcp(uint32_t lo_bits, uint32_t hi_bits, uint64_t* mismatches, uint32_t* first_bad) {
+  if (!mismatches || !first_bad || hi_bits < lo_bits) return fail(CBP_EINVAL, "invalid self-test range");
+  int dev;
+  int rc = current_device(&dev);
+  if (rc) return rc;
+  unsigned long long* d = nullptr;
+  CK(cudaMalloc(&d, 2 * sizeof(unsigned long long)), "alloc");
+  unsigned long long h[2] = {0, ~0ull};
+  cudaError_t e = cudaMemcpy(d, h, sizeof(h), cudaMemcpyHostToDevice);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e == cudaSuccess) {
+    rcp_selftest_kernel<<<sms * 8, 256>>>(lo_bits, hi_bits, d);
+    e = cudaGetLastError();
   }
+  if (e == cudaSuccess) e = cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return cuda_fail(e, "rcp self-test");
+  *mismatches = h[0];
+  *first_bad = (uint32_t)std::min<unsigned long long>(h[1], 0xffffffffull);
   return CBP_OK;
 }
 
@@ -1019,12 +1186,33 @@ int cbp_fdk_filter_f32(const float* raw_dev, int64_t np, int64_t nh, int64_t nw,
 }
 
 int cbp_release(void) {
-  std::lock_guard<std::mutex> lk(g_mu);
-  for (auto& kv : g_plans)
-    if (kv.second.mats_dev) cudaFree(kv.second.mats_dev);
-  g_plans.clear();
-  for (auto& kv : g_stats) cudaFree(kv.second);
-  g_stats.clear();
+  int dev;
+  int rc = current_device(&dev);
+  if (rc) return rc;
+  std::vector<std::shared_ptr<DevBuf>> drop;  // freed after the lock (drains the device)
+  std::vector<unsigned long long*> stats;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (auto it = g_plans.begin(); it != g_plans.end();) {
+      if (it->first.device == dev) {
+        drop.push_back(it->second.mats);
+        it = g_plans.erase(it);
+      } else {
+        ++it;
+      }
+    }
+    for (auto it = g_stats.begin(); it != g_stats.end();) {
+      if (it->first.first == dev) {
+        stats.push_back(it->second);
+        it = g_stats.erase(it);
+      } else {
+        ++it;
+      }
+    }
+  }
+  drop.clear();
+  CK(cudaDeviceSynchronize(), "release: device sync");
+  for (auto p : stats) cudaFree(p);
   return CBP_OK;
 }
 
@@ -1032,6 +1220,241 @@ int cbp_last_plan(int64_t* out9) {
   if (!out9) return fail(CBP_EINVAL, "null buffer");
   std::memcpy(out9, g_last_plan, sizeof(g_last_plan));
   return CBP_OK;
+}
+
+}  // extern "C"
+
+// ============================================================ multi-GPU band transport
+// The z-slab driver moves detector-row bands with the copy engines (cudaMemcpy3DPeerAsync
+// over NVLink / NVSwitch), never with SM kernels: the root's SMs stay on its own slab.
+namespace {
+
+typedef CUresult (*GetAddressRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+GetAddressRangeFn get_address_range() {
+  static GetAddressRangeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<GetAddressRangeFn>(p);
+  });
+  return fn;
+}
+
+// angles [s0, s1) x rows [v0, v0+rows) of a NATURAL stack on device src_dev -> staging layout
+// [s1-s0][rows][pitch] on dst_dev (copy engines; the pad columns [nw, pitch) are not written)
+int copy_band(const float* img, int src_dev, int64_t nh, int64_t nw, int64_t s0, int64_t s1, int64_t v0,
+              int64_t rows, float* dst, int dst_dev, int64_t pitch, cudaStream_t st) {
+  cudaMemcpy3DPeerParms cp;
+  std::memset(&cp, 0, sizeof(cp));
+  cp.srcPtr = make_cudaPitchedPtr(const_cast<float*>(img + ((size_t)s0 * nh + v0) * nw), (size_t)nw * 4, (size_t)nw,
+                                  (size_t)nh);
+  cp.srcDevice = src_dev;
+  cp.dstPtr = make_cudaPitchedPtr(dst, (size_t)pitch * 4, (size_t)nw, (size_t)rows);
+  cp.dstDevice = dst_dev;
+  cp.extent = make_cudaExtent((size_t)nw * 4, (size_t)rows, (size_t)(s1 - s0));
+  CK(cudaMemcpy3DPeerAsync(&cp, st), "band copy (cudaMemcpy3DPeerAsync)");
+  return CBP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cbp_copy_band(const float* img_dev, int src_device, int64_t np, int64_t nh, int64_t nw, int64_t s0, int64_t s1,
+                  int64_t v0, int64_t rows, float* dst_dev, int64_t pitch, void* cuda_stream) {
+  if (!img_dev || !dst_dev) return fail(CBP_EINVAL, "null buffer");
+  if (np < 1 || nh < 1 || nw < 1 || s0 < 0 || s1 > np || s0 >= s1 || v0 < 0 || rows < 1 || v0 + rows > nh ||
+      pitch < nw || (pitch & 3))
+    return fail(CBP_EINVAL, "invalid band copy");
+  int dev;
+  int rc = current_device(&dev);
+  if (rc) return rc;
+  if (src_device < 0) {  // the device that owns the source (local, peer or IPC-mapped memory)
+    cudaPointerAttributes a;
+    CK(cudaPointerGetAttributes(&a, img_dev), "cudaPointerGetAttributes(band source)");
+    src_device = a.type == cudaMemoryTypeDevice ? a.device : dev;
+  }
+  return copy_band(img_dev, src_device, nh, nw, s0, s1, v0, rows, dst_dev, dev, pitch,
+                   static_cast<cudaStream_t>(cuda_stream));
+}
+
+int cbp_ipc_export(const void* dev_ptr, void* handle64, int64_t* offset) {
+  if (!dev_ptr || !handle64 || !offset) return fail(CBP_EINVAL, "null buffer");
+  GetAddressRangeFn range = get_address_range();
+  if (!range) return fail(CBP_ECUDA, "cuMemGetAddressRange unavailable from the driver");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+    return fail(CBP_EINVAL, "not a device allocation");
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)), "cudaIpcGetMemHandle");
+  std::memcpy(handle64, &h, sizeof(h));
+  *offset = (int64_t)(reinterpret_cast<CUdeviceptr>(dev_ptr) - base);
+  return CBP_OK;
+}
+
+int cbp_ipc_open(const void* handle64, int64_t offset, void** dev_ptr) {
+  if (!handle64 || !dev_ptr || offset < 0) return fail(CBP_EINVAL, "null buffer");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof(h));
+  void* base = nullptr;
+  CK(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  *dev_ptr = static_cast<char*>(base) + offset;
+  return CBP_OK;
+}
+
+int cbp_ipc_close(void* dev_ptr, int64_t offset) {
+  if (!dev_ptr) return fail(CBP_EINVAL, "null buffer");
+  CK(cudaIpcCloseMemHandle(static_cast<char*>(dev_ptr) - offset), "cudaIpcCloseMemHandle");
+  return CBP_OK;
+}
+
+int cbp_backproject_multi(const float* img_dev, int64_t np, int64_t nh, int64_t nw, const float* mats_host,
+                          float* const* slab_dev, int64_t nx, int64_t ny, int64_t nz, const int64_t* k_bounds,
+                          int n_gpus, const int* devices, int variant, unsigned flags, int64_t n_chunks,
+                          int64_t* stats5) {
+  int rc = check_dims(np, nh, nw, nx, ny, nz);
+  if (rc) return rc;
+  if (!img_dev || !mats_host || !slab_dev || !k_bounds || !devices || n_gpus < 1)
+    return fail(CBP_EINVAL, "null buffer or no devices");
+  if (variant < 0 || variant > 5) return fail(CBP_EINVAL, "unknown kernel variant");
+  if (v_mirror(variant) && (nz & 1)) return fail(CBP_EINVAL, "symmetry kernels need an even nz");
+  if (k_bounds[0] != 0 || k_bounds[n_gpus] != nz) return fail(CBP_EINVAL, "k_bounds must span [0, nz]");
+  for (int r = 0; r < n_gpus; ++r) {
+    if (k_bounds[r + 1] < k_bounds[r]) return fail(CBP_EINVAL, "k_bounds must be non-decreasing");
+    if (k_bounds[r + 1] > k_bounds[r] && !slab_dev[r]) return fail(CBP_EINVAL, "null slab buffer");
+  }
+  if (!mats_finite(mats_host, np * 12)) return fail(CBP_EINVAL, "projection matrices contain non-finite values");
+  if (stats5)
+    for (int q = 0; q < 5; ++q) stats5[q] = 0;
+  if (samples_nothing(nh, nw)) return CBP_OK;
+  int caller_dev;
+  rc = current_device(&caller_dev);
+  if (rc) return rc;
+  n_chunks = std::max<int64_t>(1, std::min<int64_t>(n_chunks <= 0 ? 8 : n_chunks, np));
+  const int root = devices[0];
+  const int64_t pitch = cbp_staged_pitch(nw);
+  const bool root_direct = (nw & 3) == 0;  // rank 0 reads the NATURAL stack in place
+
+  struct Rank {
+    int dev = -1;
+    int64_t k0 = 0, k1 = 0, v0 = 0, rows = 0, cap = 0;
+    cudaStream_t copy = nullptr, comp = nullptr;
+    cudaEvent_t copied[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr};
+    float* buf[2] = {nullptr, nullptr};
+    ScopedStats stats;
+  };
+  std::vector<Rank> R((size_t)n_gpus);
+  auto fin = [&](int code) {
+    for (auto& r : R) {
+      if (r.dev < 0) continue;
+      cudaSetDevice(r.dev);
+      if (r.comp) cudaStreamSynchronize(r.comp);
+      if (r.copy) cudaStreamSynchronize(r.copy);
+      r.stats.release(r.comp);
+      for (int b = 0; b < 2; ++b)
+        if (r.buf[b]) cudaFreeAsync(r.buf[b], r.comp);
+      if (r.comp) cudaStreamSynchronize(r.comp);
+      for (int b = 0; b < 2; ++b) {
+        if (r.copied[b]) cudaEventDestroy(r.copied[b]);
+        if (r.done[b]) cudaEventDestroy(r.done[b]);
+      }
+      if (r.copy) cudaStreamDestroy(r.copy);
+      if (r.comp) cudaStreamDestroy(r.comp);
+    }
+    cudaSetDevice(caller_dev);
+    return code;
+  };
+  // prior work on every participating device (the projections on the root, zeroed or
+  // accumulated slabs elsewhere) lands before the first copy or launch: the call is a
+  // synchronous whole-job entry point
+  for (int r = 0; r < n_gpus; ++r) {
+    CK(cudaSetDevice(devices[r]), "cudaSetDevice");
+    CK(cudaDeviceSynchronize(), "multi: device sync");
+  }
+  for (int r = 0; r < n_gpus; ++r) {
+    Rank& q = R[(size_t)r];
+    q.dev = devices[r];
+    q.k0 = k_bounds[r];
+    q.k1 = k_bounds[r + 1];
+    if (q.k1 <= q.k0) continue;
+    slab_vrange(mats_host, np, nh, nw, nx, ny, nz, variant, q.k0, q.k1, &q.v0, &q.rows);
+    if (q.rows == 0) continue;
+    cudaError_t e = cudaSetDevice(q.dev);
+    if (e == cudaSuccess && q.dev != root) {
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, q.dev, root);
+      if (can) {
+        cudaError_t pe = cudaDeviceEnablePeerAccess(root, 0);
+        if (pe == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      }
+    }
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&q.comp, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&q.copy, cudaStreamNonBlocking);
+    for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+      e = cudaEventCreateWithFlags(&q.copied[b], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&q.done[b], cudaEventDisableTiming);
+    }
+    if (e != cudaSuccess) return fin(cuda_fail(e, "multi: stream/event setup"));
+    keep_pool_warm(q.dev);
+    if ((rc = q.stats.alloc(q.comp))) return fin(rc);
+    if (!(r == 0 && root_direct)) {
+      q.cap = ceil_div(np, n_chunks);
+      for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+        const size_t bytes = (size_t)q.cap * q.rows * pitch * 4;
+        e = cudaMallocAsync(reinterpret_cast<void**>(&q.buf[b]), bytes, q.comp);
+        if (e == cudaSuccess) e = cudaMemsetAsync(q.buf[b], 0, bytes, q.comp);  // pad columns stay zero
+      }
+      if (e == cudaSuccess) e = cudaEventRecord(q.done[0], q.comp);  // buffers ready for the first copies
+      if (e == cudaSuccess) e = cudaEventRecord(q.done[1], q.comp);
+      if (e != cudaSuccess) return fin(cuda_fail(e, "multi: band buffers"));
+    }
+  }
+  // chunk c of every rank before chunk c+1 of any: copy c+1 overlaps compute c
+  for (int64_t c = 0; c < n_chunks; ++c) {
+    const int64_t s0 = np * c / n_chunks, s1 = np * (c + 1) / n_chunks;
+    const int b = (int)(c & 1);
+    for (int r = 0; r < n_gpus; ++r) {
+      Rank& q = R[(size_t)r];
+      if (q.k1 <= q.k0 || q.rows == 0) continue;
+      CK(cudaSetDevice(q.dev), "cudaSetDevice");
+      StagedCall call{img_dev, nw, np, nh, nw, 0, nh, mats_host, slab_dev[r], CBP_NATURAL, nx, ny, q.k1 - q.k0, q.k0,
+                      nz, s0, s1, 0, np, variant, flags};
+      if (q.buf[0]) {
+        cudaError_t e = cudaStreamWaitEvent(q.copy, q.done[b], 0);  // compute c-2 released the buffer
+        if (e != cudaSuccess) return fin(cuda_fail(e, "multi: wait"));
+        if ((rc = copy_band(img_dev, root, nh, nw, s0, s1, q.v0, q.rows, q.buf[b], q.dev, pitch, q.copy)))
+          return fin(rc);
+        e = cudaEventRecord(q.copied[b], q.copy);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(q.comp, q.copied[b], 0);
+        if (e != cudaSuccess) return fin(cuda_fail(e, "multi: events"));
+        call.staged = q.buf[b];
+        call.pitch = pitch;
+        call.band_v0 = q.v0;
+        call.band_rows = q.rows;
+        call.s_base = s0;
+        call.n_staged = s1 - s0;
+      }
+      if ((rc = launch_staged(call, q.stats.d, q.comp))) return fin(rc);
+      if (q.buf[0]) {
+        cudaError_t e = cudaEventRecord(q.done[b], q.comp);
+        if (e != cudaSuccess) return fin(cuda_fail(e, "multi: events"));
+      }
+    }
+  }
+  for (auto& q : R) {
+    if (q.k1 <= q.k0 || q.rows == 0) continue;
+    CK(cudaSetDevice(q.dev), "cudaSetDevice");
+    int64_t st5[5] = {0, 0, 0, 0, 0};
+    const int rr = read_stats(q.stats.d, q.comp, st5);
+    if (stats5)
+      for (int k = 0; k < 5; ++k) stats5[k] += st5[k];
+    if (rr && !rc) rc = rr;
+  }
+  return fin(rc);
 }
 
 }  // extern "C"

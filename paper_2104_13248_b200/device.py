@@ -14,7 +14,9 @@ from . import _lib
 from .backprojector import KernelVariant
 from .tensors import Layout
 
-__all__ = ["StagedProjections", "backproject_device", "backproject_staged", "sync_status", "last_plan", "stream_handle"]
+__all__ = ["StagedProjections", "backproject_device", "backproject_staged", "backproject_window", "backproject_multi",
+           "copy_band", "ipc_export", "ipc_open", "ipc_close", "selftest_rcp", "sync_status", "last_plan",
+           "stream_handle"]
 
 
 def _torch():
@@ -90,6 +92,104 @@ def backproject_staged(staged: StagedProjections, mats: np.ndarray, vol_dev, nx:
         staged.data.data_ptr(), staged.pitch, staged.np, staged.nh, staged.nw, staged.v0, staged.rows,
         _lib.f32ptr(mats), vol_dev.data_ptr(), 0 if vol_layout is Layout.NATURAL else 1, nx, ny, nz, k0, nz_total,
         s_begin, s_end, int(KernelVariant(variant)), flags, stream_handle(stream)))
+
+
+def backproject_window(band_dev, s_base: int, mats: np.ndarray, vol_dev, n_proj: int, nh: int, nw: int, v0: int,
+                       rows: int, nx: int, ny: int, nz: int, variant: KernelVariant = KernelVariant.BASELINE,
+                       k0: int = 0, nz_total: int | None = None, s_begin: int | None = None,
+                       s_end: int | None = None, vol_layout: Layout = Layout.NATURAL, flags: int = 0,
+                       stream=None) -> None:
+    """Accumulate angles [s_begin, s_end) from a band buffer holding only angles
+    [s_base, s_base + band_dev.shape[0]) (layout [n][rows][pitch]) into slab [k0, k0+nz)."""
+    vol_layout = Layout(vol_layout)
+    torch = _torch()
+    if not (isinstance(band_dev, torch.Tensor) and band_dev.is_cuda and band_dev.dtype == torch.float32
+            and band_dev.is_contiguous() and band_dev.dim() == 3 and band_dev.shape[1] == rows):
+        raise ValueError("band must be a contiguous float32 CUDA tensor [n][rows][pitch]")
+    _check_tensor(vol_dev, _vol_shape(nx, ny, nz, vol_layout), "volume")
+    mats = np.ascontiguousarray(mats, dtype=np.float32)
+    if mats.shape != (n_proj, 3, 4):
+        raise ValueError(f"expected ({n_proj}, 3, 4) matrices, got {mats.shape}")
+    n = int(band_dev.shape[0])
+    s_begin = s_base if s_begin is None else s_begin
+    s_end = s_base + n if s_end is None else s_end
+    nz_total = nz if nz_total is None else nz_total
+    _lib.check(_lib.lib().cbp_backproject_window(
+        band_dev.data_ptr(), int(band_dev.shape[2]), n_proj, nh, nw, v0, rows, s_base, n, _lib.f32ptr(mats),
+        vol_dev.data_ptr(), 0 if vol_layout is Layout.NATURAL else 1, nx, ny, nz, k0, nz_total, s_begin, s_end,
+        int(KernelVariant(variant)), flags, stream_handle(stream)))
+
+
+def copy_band(src_ptr: int, n_proj: int, nh: int, nw: int, s0: int, s1: int, v0: int, rows: int, dst_dev,
+              src_device: int = -1, stream=None) -> None:
+    """Copy-engine transfer of angles [s0, s1) x rows [v0, v0+rows) of a NATURAL stack at
+    device address ``src_ptr`` (local or IPC-mapped) into ``dst_dev`` [s1-s0][rows][pitch]."""
+    _lib.check(_lib.lib().cbp_copy_band(src_ptr, src_device, n_proj, nh, nw, s0, s1, v0, rows, dst_dev.data_ptr(),
+                                        int(dst_dev.shape[2]), stream_handle(stream)))
+
+
+def ipc_export(t) -> tuple[bytes, int]:
+    """(64-byte CUDA IPC handle of t's allocation, byte offset of t in it)."""
+    import ctypes
+
+    h = ctypes.create_string_buffer(64)
+    off = np.zeros(1, np.int64)
+    _lib.check(_lib.lib().cbp_ipc_export(t.data_ptr(), h, _lib.i64ptr(off)))
+    return bytes(h.raw), int(off[0])
+
+
+def ipc_open(handle: bytes, offset: int) -> int:
+    import ctypes
+
+    p = ctypes.c_void_p()
+    _lib.check(_lib.lib().cbp_ipc_open(ctypes.create_string_buffer(handle, 64), offset, ctypes.byref(p)))
+    return int(p.value)
+
+
+def ipc_close(ptr: int, offset: int) -> None:
+    _lib.check(_lib.lib().cbp_ipc_close(ptr, offset))
+
+
+def backproject_multi(img_dev, mats: np.ndarray, slabs: list, k_bounds, nx: int, ny: int, nz: int,
+                      devices: list[int] | None = None, variant: KernelVariant = KernelVariant.BASELINE,
+                      n_chunks: int = 8, flags: int = 0) -> dict:
+    """Single-process multi-GPU z-slab back-projection (cbp_backproject_multi): ``img_dev``
+    NATURAL on devices[0], ``slabs[r]`` the NATURAL slab tensor of rank r on devices[r]
+    (``None`` for empty slabs).  Synchronous; returns the summed status counters."""
+    import ctypes
+
+    n = len(slabs)
+    devices = [s.device.index if s is not None else 0 for s in slabs] if devices is None else list(devices)
+    if len(devices) != n or len(k_bounds) != n + 1:
+        raise ValueError("need one device and one slab per rank and n_ranks + 1 slice bounds")
+    n_proj, nh, nw = (int(v) for v in img_dev.shape)
+    _check_tensor(img_dev, (n_proj, nh, nw), "projections")
+    for r, t in enumerate(slabs):
+        depth = int(k_bounds[r + 1]) - int(k_bounds[r])
+        if depth > 0:
+            _check_tensor(t, (depth, ny, nx), f"slab {r}")
+    mats = np.ascontiguousarray(mats, dtype=np.float32)
+    ptrs = (ctypes.c_void_p * n)(*[t.data_ptr() if t is not None else 0 for t in slabs])
+    devs = (ctypes.c_int * n)(*devices)
+    kb = np.ascontiguousarray(np.asarray(k_bounds, dtype=np.int64))
+    st = np.zeros(5, np.int64)
+    rc = _lib.lib().cbp_backproject_multi(img_dev.data_ptr(), n_proj, nh, nw, _lib.f32ptr(mats), ptrs, nx, ny, nz,
+                                          _lib.i64ptr(kb), n, devs, int(KernelVariant(variant)), flags, n_chunks,
+                                          _lib.i64ptr(st))
+    stats = {"smem_pairs": int(st[0]), "global_pairs": int(st[1]), "skipped_pairs": int(st[2]),
+             "band_violations": int(st[3]), "box_misses": int(st[4])}
+    _lib.check(rc)
+    return stats
+
+
+def selftest_rcp(lo_bits: int, hi_bits: int) -> tuple[int, int]:
+    """(mismatches, first mismatching bit pattern) of rcp_rn_normal vs __frcp_rn."""
+    import ctypes
+
+    n = ctypes.c_uint64()
+    first = ctypes.c_uint32()
+    _lib.check(_lib.lib().cbp_selftest_rcp(lo_bits, hi_bits, ctypes.byref(n), ctypes.byref(first)))
+    return int(n.value), int(first.value)
 
 
 def backproject_device(img_dev, mats: np.ndarray, vol_dev, n_proj: int, nh: int, nw: int, nx: int, ny: int, nz: int,

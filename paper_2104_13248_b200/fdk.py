@@ -25,7 +25,7 @@ from . import _lib
 from .backprojector import KernelVariant
 from .tensors import Layout, ProjectionStack, Volume
 
-__all__ = ["ramp_tau", "filter_projections", "fdk_reconstruct", "fdk_scale"]
+__all__ = ["ramp_tau", "filter_projections", "fdk_reconstruct", "fdk_scale", "check_full_orbit"]
 
 
 def ramp_tau(geom) -> float:
@@ -55,8 +55,25 @@ def filter_projections(img_dev, geom, stream=None):
     return StagedProjections.wrap(out, geom.np, geom.nh, geom.nw, 0, geom.nh)
 
 
+def check_full_orbit(geom, rtol: float = 1e-6) -> None:
+    """FDK's pi * d^2 / np scale assumes angles evenly spaced over a whole turn (each ray
+    measured twice, no redundancy weighting).  Short scans (e.g. config 2's 200 degrees)
+    need Parker weights, which this module does not implement: they are rejected."""
+    a = np.sort(np.mod(np.asarray(geom.angles, dtype=np.float64), 2.0 * math.pi))
+    n = a.size
+    if n < 2:
+        raise ValueError("FDK needs projections over a full 360-degree orbit (got one angle)")
+    gaps = np.diff(np.concatenate([a, [a[0] + 2.0 * math.pi]]))
+    step = 2.0 * math.pi / n
+    if np.abs(gaps - step).max() > max(rtol * 2.0 * math.pi, 1e-9) + 1e-6 * step:
+        raise ValueError("fdk_reconstruct needs angles evenly spaced over a full 360-degree orbit "
+                         "(short scans need Parker weighting, which is not implemented)")
+
+
 def fdk_reconstruct(proj: ProjectionStack, geom, mats: np.ndarray | None = None) -> Volume:
-    """Raw (unfiltered) NATURAL projections -> FDK volume (host in, host out)."""
+    """Raw (unfiltered) NATURAL projections -> FDK volume (host in, host out).
+
+    Full circular orbits only (``check_full_orbit``)."""
     import torch
 
     from .device import backproject_staged, sync_status
@@ -66,6 +83,7 @@ def fdk_reconstruct(proj: ProjectionStack, geom, mats: np.ndarray | None = None)
         raise ValueError("fdk_reconstruct expects NATURAL projections")
     if (proj.np, proj.nh, proj.nw) != (geom.np, geom.nh, geom.nw):
         raise ValueError("projection stack does not match the geometry")
+    check_full_orbit(geom)
     mats = projection_matrices(geom) if mats is None else np.ascontiguousarray(mats, np.float32)
     img = torch.from_numpy(proj.data).cuda()
     staged = filter_projections(img, geom)

@@ -103,3 +103,18 @@ def test_counter_errors_and_ratios():
     assert count_ops(KernelVariant.BASELINE, 64, 64, 64, 64).dot_ops == 3 * 64 ** 4
     assert dot_reduction_ratio(256) == pytest.approx(1 - 130 / 768)
     assert asymptotic_dot_reduction_ratio(1 << 20) == pytest.approx(5 / 6, rel=1e-5)
+
+
+def test_fdk_rejects_short_scans():
+    """fdk_reconstruct's pi*d^2/np scale is only right for a full, evenly sampled orbit."""
+    import math
+
+    from paper_2104_13248_b200 import geometry as G
+    from paper_2104_13248_b200.fdk import check_full_orbit
+
+    full = G.build_geometry(nx=8, ny=8, nz=8, nw=16, nh=16, np=12)
+    check_full_orbit(full)
+    short = G.build_geometry(nx=8, ny=8, nz=8, nw=16, nh=16, np=12,
+                             angles=[s * math.radians(200.0) / 12 for s in range(12)])
+    with pytest.raises(ValueError, match="360"):
+        check_full_orbit(short)

@@ -84,3 +84,4 @@ def test_fdk_reconstruction_recovers_the_phantom(torch_cuda):
     assert abs(float(rec.mean()) - float(inner.mean())) < 0.08 * float(inner.mean())
     outside = vol.data[:, :4, :4]
     assert abs(float(outside.mean())) < 0.1
+

@@ -326,3 +326,19 @@ def test_awkward_medium_sizes_bitwise(torch_cuda, jitter, path):
     oracle.baseline(img, mats, ref)
     assert out.tobytes() == ref.tobytes()
     assert stats["smem_pairs"] > 0
+
+
+@pytest.mark.parametrize("nh,nw", [(1, 16), (16, 1), (1, 1)])
+def test_degenerate_detector_samples_nothing(torch_cuda, nh, nw):
+    """A 1-pixel-high or -wide detector is legal in the reference (sizes >= 1,
+    tensors.py:44-58) and samples nothing (guard x < nw-1, y < nh-1, _kernels.py:52):
+    every entry point leaves the volume bitwise unchanged."""
+    t = load_golden("tiny")
+    n_proj = t["mats"].shape[0]
+    start = np.random.default_rng(3).normal(size=(12, 12, 12)).astype(np.float32)
+    img = np.ones((n_proj, nh, nw), np.float32)
+    v = Volume.from_array(start.copy())
+    backproject_baseline(ProjectionStack.from_array(img), t["mats"], v)
+    assert v.data.tobytes() == start.tobytes()
+    out, _ = run_device(torch_cuda, img, t["mats"], start, KernelVariant.BASELINE, Layout.NATURAL, Layout.NATURAL, 0)
+    assert out.tobytes() == start.tobytes()

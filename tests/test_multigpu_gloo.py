@@ -25,7 +25,7 @@ def free_port() -> int:
 
 
 class OracleBackend:
-    """CPU stand-in for slabs.CudaBackend (same interface)."""
+    """CPU stand-in for slabs.CudaBackend (same interface, p2p transport)."""
 
     def __init__(self, torch):
         self.torch = torch
@@ -34,21 +34,26 @@ class OracleBackend:
     def empty_band(self, n_proj, nw, rows):
         from paper_2104_13248_b200.slabs import pitch_of
 
-        return self.torch.empty((n_proj, rows, pitch_of(nw)), dtype=self.torch.float32)
-
-    def stage_band(self, img, plan, v0, rows, out):
-        out.zero_()
-        out[:, :, : plan.nw] = img[:, v0:v0 + rows, :]
+        return self.torch.zeros((n_proj, rows, pitch_of(nw)), dtype=self.torch.float32)
 
     def empty_slab(self, plan, k0, k1):
         return self.torch.zeros((k1 - k0, plan.ny, plan.nx), dtype=self.torch.float32)
 
-    def compute(self, band, plan, v0, rows, k0, k1, s0, s1, mats, vol):
+    def direct(self, img, plan):
+        return img if plan.nw % 4 == 0 else None
+
+    def stage_chunk(self, img, plan, v0, rows, s0, s1, out):
+        out[: s1 - s0, :, : plan.nw] = img[s0:s1, v0:v0 + rows, :]
+
+    def compute(self, band, s_base, plan, v0, rows, k0, k1, s0, s1, mats, vol):
         import oracle
 
-        img = np.ascontiguousarray(band[s0:s1, :, : plan.nw].numpy())
-        v = vol.numpy()
-        self.violations += oracle.baseline(img, mats[s0:s1], v, threads=1, nh=plan.nh, v0=v0, k_lo=k0)
+        img = np.ascontiguousarray(band[s0 - s_base:s1 - s_base, :, : plan.nw].numpy())
+        self.violations += oracle.baseline(img, mats[s0:s1], vol.numpy(), threads=1, nh=plan.nh, v0=v0, k_lo=k0)
+
+    def check(self):
+        if self.violations:
+            raise RuntimeError(f"{self.violations} samples outside the band")
 
 
 def worker(rank, world, port, case, n_chunks, result_q):
