@@ -209,6 +209,24 @@ const void* tiled_kernel_ptr(int variant, bool gen, int c, bool check) {
   return check ? tiled_kernel_ptr_c<true>(variant, gen, c) : tiled_kernel_ptr_c<false>(variant, gen, c);
 }
 
+// tolerance mode (CBP_FLAG_FMA_LERP): baseline arithmetic with FMA lerps
+template <bool GEN, int C>
+const void* fmalerp_fn() {
+  return reinterpret_cast<const void*>(
+      &bp_tiled_fmalerp_kernel<V_BASELINE, GEN, kTiles[C].NWX, kTiles[C].NWY, kTiles[C].MINB>);
+}
+template <bool GEN>
+const void* fmalerp_by_tile(int c) {
+  switch (c) {
+    case 0: return fmalerp_fn<GEN, 0>();
+    case 1: return fmalerp_fn<GEN, 1>();
+    case 3: return fmalerp_fn<GEN, 3>();
+    case 4: return fmalerp_fn<GEN, 4>();
+    case 5: return fmalerp_fn<GEN, 5>();
+    default: return fmalerp_fn<GEN, 2>();
+  }
+}
+
 const void* naive_kernel_ptr(int variant) {
   switch (variant) {
     case V_BASELINE: return reinterpret_cast<const void*>(&bp_naive_kernel<V_BASELINE>);
@@ -501,6 +519,9 @@ int validate_staged(StagedCall& c) {
   if (c.s_base < 0 || c.s_base > c.s_begin || c.s_base + c.n_staged < c.s_end || c.s_base + c.n_staged > c.np)
     return fail(CBP_EINVAL, "staged angle window does not cover [s_begin, s_end)");
   if (!mats_finite(c.mats_host, c.np * 12)) return fail(CBP_EINVAL, "projection matrices contain non-finite values");
+  if ((c.flags & CBP_FLAG_FMA_LERP) &&
+      (c.variant != V_BASELINE || (c.flags & (CBP_FLAG_NAIVE | CBP_FLAG_CHECK | CBP_FLAG_NO_SMEM))))
+    return fail(CBP_EINVAL, "CBP_FLAG_FMA_LERP is a tolerance mode of the tiled baseline kernel only");
   if (samples_nothing(c.nh, c.nw)) return CBP_OK;
   if (c.band_v0 < 0 || c.band_rows < 2 || c.band_v0 + c.band_rows > c.nh || c.pitch < c.nw || (c.pitch & 3))
     return fail(CBP_EINVAL, "invalid detector-row band or pitch");
@@ -574,7 +595,9 @@ int launch_staged(StagedCall c, unsigned long long* stats, cudaStream_t st) {
                   plan.hb, (long long)c.pitch);
     return fail(CBP_ECUDA, buf);
   }
-  const void* fn = tiled_kernel_ptr(key.variant, plan.kind == 2, plan.cfg, (c.flags & CBP_FLAG_CHECK) != 0);
+  const void* fn = (c.flags & CBP_FLAG_FMA_LERP)
+                       ? (plan.kind == 2 ? fmalerp_by_tile<true>(plan.cfg) : fmalerp_by_tile<false>(plan.cfg))
+                       : tiled_kernel_ptr(key.variant, plan.kind == 2, plan.cfg, (c.flags & CBP_FLAG_CHECK) != 0);
   rc = ensure_smem(dev, fn, plan.smem);
   if (rc) return rc;
   const int64_t blocks = (int64_t)p.tiles_x * p.tiles_y * p.tiles_z;

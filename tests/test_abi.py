@@ -74,4 +74,6 @@ def test_no_fma_contraction_in_backprojection_sass():
         if "bp_tiled_kernel" in name or "bp_naive_kernel" in name:
             checked += 1
             assert "FFMA2" not in f, name
+        if "bp_tiled_fmalerp_kernel" in name:  # the opt-in tolerance mode does fuse its lerps
+            assert "FFMA2" in f, name
     assert checked > 0
