@@ -1,0 +1,79 @@
+"""Run the reference package's OWN tests with its kernel seam served by the GPU library.
+
+    python tools/run_reference_tests.py [pytest args...]
+
+Needs the reference installed into baseline/_ref and its test directory copied
+to baseline/_ref_tests (tools/install_reference.sh does both, in the build
+container; both directories are git-ignored and travel to the GPU box).  The
+reference's conftest/helpers are used unmodified; a pytest plugin installs
+``paper_2104_13248_b200.seam`` before any test runs, so every
+``backproject_baseline`` / ``backproject_optimized`` call in those tests
+executes on the B200 (the numba kernels are never called), and the run fails
+if the seam was not exercised.  Writes a summary JSON to
+gpurun_out/reference_tests_on_gpu.json.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parents[1]
+REF = REPO / "baseline" / "_ref"
+REF_TESTS = REPO / "baseline" / "_ref_tests"
+
+DEFAULT_FILES = ["test_backprojector.py", "test_counters.py", "test_bench.py", "test_acceptance.py"]
+
+
+class SeamPlugin:
+    def __init__(self):
+        self.outcomes = {}
+
+    def pytest_sessionstart(self, session):
+        import conebp
+
+        from paper_2104_13248_b200 import seam
+
+        seam.install(conebp)
+        # numba must not be reachable through the seam any more
+        assert conebp._kernels.baseline.__module__ == "paper_2104_13248_b200.seam"
+
+    def pytest_runtest_logreport(self, report):
+        if report.when == "call" or report.outcome != "passed":
+            self.outcomes[report.nodeid] = report.outcome
+
+
+def main(argv: list[str]) -> int:
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/conebp_numba_cache")
+    for p in (str(REF), str(REPO)):
+        sys.path.insert(0, p)
+    if not REF_TESTS.is_dir():
+        print(f"{REF_TESTS} missing: run tools/install_reference.sh in the build container", file=sys.stderr)
+        return 2
+    import pytest
+
+    from paper_2104_13248_b200 import seam
+
+    plugin = SeamPlugin()
+    files = [str(REF_TESTS / f) for f in DEFAULT_FILES if (REF_TESTS / f).exists()]
+    args = ["-q", "-p", "no:cacheprovider", "--rootdir", str(REF_TESTS), *argv, *files]
+    rc = pytest.main(args, plugins=[plugin])
+    passed = sum(v == "passed" for v in plugin.outcomes.values())
+    failed = sorted(k for k, v in plugin.outcomes.items() if v == "failed")
+    summary = {"pytest_exit": int(rc), "passed": passed, "failed": failed,
+               "skipped": sum(v == "skipped" for v in plugin.outcomes.values()),
+               "seam_calls": dict(seam.calls), "files": [Path(f).name for f in files]}
+    out = REPO / "gpurun_out"
+    out.mkdir(exist_ok=True)
+    (out / "reference_tests_on_gpu.json").write_text(json.dumps(summary, indent=1))
+    print(json.dumps(summary))
+    if sum(seam.calls.values()) == 0:
+        print("the GPU seam was never called", file=sys.stderr)
+        return 3
+    return int(rc)
+
+
+if __name__ == "__main__":
+    sys.exit(main(sys.argv[1:]))
