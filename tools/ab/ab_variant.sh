@@ -1,4 +1,4 @@
-# build the working tree with extra nvcc flags into ab/<name>:  tools/ab_variant.sh NAME "-DFOO=1"
+# build the working tree with extra nvcc flags into ab/<name>:  tools/ab/ab_variant.sh NAME "-DFOO=1"
 set -e
 name=$1; extra=$2
 d=/tmp/var_$name; rm -rf $d; mkdir -p $d

@@ -15,6 +15,7 @@ ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--variant", default="baseline")
 ap.add_argument("--flags", type=int, default=0)
 ap.add_argument("--uniform", action="store_true", help="uniform inputs instead of the phantom (faster setup)")
+ap.add_argument("--slab", default=None, help="k0:k1 -- back-project only this z-slab (global indices; for ncu on cfg4)")
 a = ap.parse_args()
 spec = configs.get_config(a.config)
 geom = spec.geometry()
@@ -24,14 +25,15 @@ if a.uniform:
 else:
     img = spec.projections_device(geom, device="cuda")
 st = D.StagedProjections(img, geom.np, geom.nh, geom.nw)
-vol = torch.zeros((geom.nz, geom.ny, geom.nx), device="cuda")
+k0, k1 = (int(t) for t in a.slab.split(":")) if a.slab else (0, geom.nz)
+vol = torch.zeros((k1 - k0, geom.ny, geom.nx), device="cuda")
 v = KernelVariant.parse(a.variant)
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * a.iters)]
 for i in range(a.iters):
     ev[2 * i].record()
-    D.backproject_staged(st, mats, vol, geom.nx, geom.ny, geom.nz, v, flags=a.flags)
+    D.backproject_staged(st, mats, vol, geom.nx, geom.ny, k1 - k0, v, k0=k0, nz_total=geom.nz, flags=a.flags)
     ev[2 * i + 1].record()
 torch.cuda.synchronize()
 ms = [ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(a.iters)]
 print("plan", D.last_plan(), "stats", D.sync_status())
-print("ms", [round(x, 3) for x in ms], "GUPS", [round(geom.nx * geom.ny * geom.nz * geom.np / (x * 1e6), 1) for x in ms])
+print("ms", [round(x, 3) for x in ms], "GUPS", [round(geom.nx * geom.ny * (k1 - k0) * geom.np / (x * 1e6), 1) for x in ms])
