@@ -11,7 +11,7 @@ from collections import Counter
 
 rep = sys.argv[1]
 updates = float(sys.argv[2]) if len(sys.argv) > 2 else None
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+raw = open(rep).read() if rep.endswith(".csv") else subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 hdr, units, vals = rows[0], rows[1], rows[2]
 M = {h: (v, u) for h, v, u in zip(hdr, vals, units)}

@@ -6,7 +6,7 @@ back-projected over all angles -- one rank after another on the single GPU.  The
 of the real driver never wait on each other during compute (no collective after the
 band distribution), so max over ranks of these times is the compute part of the N-GPU
 step; T1 / (N * max) is the compute-only scaling efficiency.  The band bytes each rank
-receives from rank 0 are printed as well (the NCCL payload, not timed here).
+receives from rank 0 are printed as well (the copy-engine payload, not timed here).
 
     python tools/slab_balance.py --config 4 --ranks 2 4 8
 """
@@ -26,8 +26,8 @@ from paper_2104_13248_b200 import slabs as SL
 def time_slab(img, mats, plan, v0, rows, k0, k1, n_warm=64):
     if rows == 0 or k1 == k0:
         return 0.0
-    band = torch.empty((plan.np, rows, SL.pitch_of(plan.nw)), dtype=torch.float32, device="cuda")
-    SL.CudaBackend(torch).stage_band(img, plan, v0, rows, band)
+    band = torch.zeros((plan.np, rows, SL.pitch_of(plan.nw)), dtype=torch.float32, device="cuda")
+    D.copy_band(img.data_ptr(), plan.np, plan.nh, plan.nw, 0, plan.np, v0, rows, band)
     staged = D.StagedProjections.wrap(band, plan.np, plan.nh, plan.nw, v0, rows)
     vol = torch.zeros((k1 - k0, plan.ny, plan.nx), dtype=torch.float32, device="cuda")
     D.backproject_staged(staged, mats, vol, plan.nx, plan.ny, k1 - k0, k0=k0, nz_total=plan.nz, s_end=min(n_warm, plan.np))
@@ -47,6 +47,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--ranks", type=int, nargs="+", default=[2, 4, 8])
+    ap.add_argument("--align", type=int, default=32, help="slab boundary granularity in slices (16 or 32)")
     args = ap.parse_args()
     spec = configs.get_config(args.config)
     geom = spec.geometry()
@@ -55,10 +56,10 @@ def main():
     updates = geom.nx * geom.ny * geom.nz * geom.np
     plan1 = SL.plan_slabs(mats, geom.nh, geom.nw, geom.nx, geom.ny, geom.nz, 1)
     t1 = time_slab(img, mats, plan1, *plan1.bands[0], *plan1.slab(0))
-    out = {"config": args.config, "updates": updates, "t1_ms": t1, "gups_1": updates / t1 / 1e6, "runs": []}
+    out = {"config": args.config, "align": args.align, "updates": updates, "t1_ms": t1, "gups_1": updates / t1 / 1e6, "runs": []}
     print(f"cfg{args.config}: N=1 {t1:.1f} ms ({updates / t1 / 1e6:.0f} GUPS)", flush=True)
     for n in args.ranks:
-        plan = SL.plan_slabs(mats, geom.nh, geom.nw, geom.nx, geom.ny, geom.nz, n)
+        plan = SL.plan_slabs(mats, geom.nh, geom.nw, geom.nx, geom.ny, geom.nz, n, align=args.align)
         per = []
         for r in range(n):
             v0, rows = plan.bands[r]
