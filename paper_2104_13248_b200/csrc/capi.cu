@@ -771,71 +771,112 @@ int cbp_backproject_host_f32(const float* img_host, int64_t np, int64_t nh, int6
   int dev;
   rc = current_device(&dev);
   if (rc) return rc;
-  // Pipeline: projections travel host->device in angle chunks on a copy stream while
-  // the compute stream stages and back-projects the chunks already resident.  Each
-  // chunk launch accumulates angles [s0, s1) into the volume in ascending order, so
-  // the result is bitwise identical to a single launch.
-  cudaStream_t sc = nullptr, sk = nullptr;
-  CK(cudaStreamCreateWithFlags(&sc, cudaStreamNonBlocking), "stream create");
-  cudaError_t e = cudaStreamCreateWithFlags(&sk, cudaStreamNonBlocking);
-  if (e != cudaSuccess) {
-    cudaStreamDestroy(sc);
-    return cuda_fail(e, "stream create");
-  }
+  // Pipeline over three streams.  The projections travel host->device in angle chunks on
+  // the upload stream while the compute stream stages and back-projects the chunks already
+  // resident (each launch accumulates angles [s0, s1) in ascending order: bitwise identical
+  // to one launch).  A NATURAL volume is also split into z-slabs (contiguous, cut on the
+  // kernel's 32-slice z-runs): slab 0 is uploaded first, slab k+1 uploads while slab k
+  // computes and slab k downloads on the third stream while slab k+1 computes, so only
+  // the projection upload of slab 0 and the last slab's download are not hidden.
   const size_t per_proj = (size_t)nh * nw, ib = (size_t)np * per_proj * 4, vb = (size_t)nx * ny * nz * 4;
   const bool direct = img_layout == CBP_NATURAL && (nw & 3) == 0;  // natural layout is the staging layout
   const int64_t pitch = cbp_staged_pitch(nw);
-  float *img = nullptr, *vol = nullptr, *staged = nullptr;
   int64_t n_chunks = std::min<int64_t>(np, std::max<int64_t>(1, (int64_t)(ib >> 24)));  // ~16 MiB chunks
   n_chunks = std::min<int64_t>(n_chunks, 24);
   if (const char* env = std::getenv("CBP_HOST_CHUNKS")) n_chunks = std::max<int64_t>(1, std::min<int64_t>(np, std::atoi(env)));
-  keep_pool_warm(dev);
+  int64_t n_slabs = 1;
+  if (vol_layout == CBP_NATURAL && vb >= ((size_t)256 << 20)) n_slabs = std::min<int64_t>(8, nz / kZR);
+  if (const char* env = std::getenv("CBP_HOST_SLABS")) n_slabs = std::atoi(env);
+  n_slabs = std::max<int64_t>(1, std::min<int64_t>(n_slabs, ceil_div(nz, kZR)));
+  if (vol_layout != CBP_NATURAL) n_slabs = 1;  // a z-slab of [x][y][z] is not contiguous
+  std::vector<int64_t> zb((size_t)n_slabs + 1);
+  for (int64_t k = 0; k <= n_slabs; ++k) zb[k] = (k == n_slabs) ? nz : (nz * k / n_slabs) / kZR * kZR;
+  const size_t slice = (size_t)nx * ny;
+
+  cudaStream_t sc = nullptr, sk = nullptr, sd = nullptr;
+  std::vector<cudaEvent_t> ev_proj((size_t)n_chunks, nullptr), ev_vol((size_t)n_slabs, nullptr),
+      ev_done((size_t)n_slabs, nullptr);
+  float *img = nullptr, *vol = nullptr, *staged = nullptr;
   ScopedStats stats;
-  std::vector<cudaEvent_t> ev((size_t)n_chunks, nullptr);
-  e = cudaMallocAsync(reinterpret_cast<void**>(&img), ib, sk);
+  cudaError_t e = cudaStreamCreateWithFlags(&sc, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&sk, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking);
+  for (auto* v : {&ev_proj, &ev_vol, &ev_done})
+    for (auto& x : *v)
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+  keep_pool_warm(dev);
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&img), ib, sk);
   if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&vol), vb, sk);
   if (e == cudaSuccess && !direct)
     e = cudaMallocAsync(reinterpret_cast<void**>(&staged), (size_t)np * nh * pitch * 4, sk);
-  for (int64_t q = 0; q < n_chunks && e == cudaSuccess; ++q) e = cudaEventCreateWithFlags(&ev[q], cudaEventDisableTiming);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(vol, vol_host, vb, cudaMemcpyHostToDevice, sk);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(sk);  // allocations visible to the copy stream
-  if (e != cudaSuccess) rc = cuda_fail(e, "host path: allocation / volume upload");
+  if (e == cudaSuccess) e = cudaStreamSynchronize(sk);  // allocations visible to the copy streams
+  if (e != cudaSuccess) rc = cuda_fail(e, "host path: streams / allocation");
   if (rc == CBP_OK) rc = stats.alloc(sk);
+  // uploads, in the order they are needed: slab 0, the projection chunks, the other slabs
+  auto up_slab = [&](int64_t k) {
+    const size_t off = (size_t)zb[k] * slice, n = (size_t)(zb[k + 1] - zb[k]) * slice;
+    cudaError_t r = cudaMemcpyAsync(vol + off, vol_host + off, n * 4, cudaMemcpyHostToDevice, sc);
+    return r == cudaSuccess ? cudaEventRecord(ev_vol[k], sc) : r;
+  };
+  if (rc == CBP_OK && (e = up_slab(0)) != cudaSuccess) rc = cuda_fail(e, "host path: volume upload");
   for (int64_t q = 0; q < n_chunks && rc == CBP_OK; ++q) {
     const int64_t s0 = np * q / n_chunks, s1 = np * (q + 1) / n_chunks;
     e = cudaMemcpyAsync(img + s0 * per_proj, img_host + s0 * per_proj, (size_t)(s1 - s0) * per_proj * 4,
                         cudaMemcpyHostToDevice, sc);
-    if (e == cudaSuccess) e = cudaEventRecord(ev[q], sc);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(sk, ev[q], 0);
-    if (e != cudaSuccess) {
-      rc = cuda_fail(e, "host path: projection upload");
+    if (e == cudaSuccess) e = cudaEventRecord(ev_proj[q], sc);
+    if (e != cudaSuccess) rc = cuda_fail(e, "host path: projection upload");
+  }
+  for (int64_t k = 1; k < n_slabs && rc == CBP_OK; ++k)
+    if ((e = up_slab(k)) != cudaSuccess) rc = cuda_fail(e, "host path: volume upload");
+  // compute: slab 0 follows the projection chunks as they land, the others run over all angles
+  for (int64_t k = 0; k < n_slabs && rc == CBP_OK; ++k) {
+    if ((e = cudaStreamWaitEvent(sk, ev_vol[k], 0)) != cudaSuccess) {
+      rc = cuda_fail(e, "host path: wait");
       break;
     }
-    StagedCall c{img, nw, np, nh, nw, 0, nh, mats_host, vol, vol_layout, nx, ny, nz, 0, nz, s0, s1, 0, np, variant, flags};
-    if (!direct) {
-      rc = cbp_stage_projections(img + s0 * per_proj, img_layout, s1 - s0, nh, nw, 0, nh, staged + s0 * nh * pitch,
-                                 pitch, sk);
-      c.staged = staged;
-      c.pitch = pitch;
+    const int64_t k0 = zb[k], k1 = zb[k + 1];
+    float* vslab = vol + (size_t)k0 * slice;
+    for (int64_t q = 0; q < (k == 0 ? n_chunks : 1) && rc == CBP_OK; ++q) {
+      const int64_t s0 = k == 0 ? np * q / n_chunks : 0, s1 = k == 0 ? np * (q + 1) / n_chunks : np;
+      if (k == 0) {
+        if ((e = cudaStreamWaitEvent(sk, ev_proj[q], 0)) != cudaSuccess) {
+          rc = cuda_fail(e, "host path: wait");
+          break;
+        }
+        if (!direct)
+          rc = cbp_stage_projections(img + s0 * per_proj, img_layout, s1 - s0, nh, nw, 0, nh,
+                                     staged + s0 * nh * pitch, pitch, sk);
+      }
+      StagedCall c{direct ? img : staged, direct ? nw : pitch, np, nh, nw, 0, nh, mats_host, vslab, vol_layout,
+                   nx, ny, k1 - k0, k0, nz, s0, s1, 0, np, variant, flags};
+      if (rc == CBP_OK) rc = launch_staged(c, stats.d, sk);
     }
-    if (rc == CBP_OK) rc = launch_staged(c, stats.d, sk);
-  }
-  if (rc == CBP_OK) {
-    e = cudaMemcpyAsync(vol_host, vol, vb, cudaMemcpyDeviceToHost, sk);
-    if (e != cudaSuccess) rc = cuda_fail(e, "host path: copy out");
+    if (rc == CBP_OK && (e = cudaEventRecord(ev_done[k], sk)) != cudaSuccess) rc = cuda_fail(e, "host path: event");
+    // download slab k while the next slab computes
+    if (rc == CBP_OK && (e = cudaStreamWaitEvent(sd, ev_done[k], 0)) == cudaSuccess)
+      e = cudaMemcpyAsync(vol_host + (size_t)k0 * slice, vslab, (size_t)(k1 - k0) * slice * 4,
+                          cudaMemcpyDeviceToHost, sd);
+    if (rc == CBP_OK && e != cudaSuccess) rc = cuda_fail(e, "host path: copy out");
   }
   if (rc == CBP_OK) rc = read_stats(stats.d, sk, nullptr);
-  cudaStreamSynchronize(sc);
-  stats.release(sk);
-  if (img) cudaFreeAsync(img, sk);
-  if (vol) cudaFreeAsync(vol, sk);
-  if (staged) cudaFreeAsync(staged, sk);
-  e = cudaStreamSynchronize(sk);
-  if (e != cudaSuccess && rc == CBP_OK) rc = cuda_fail(e, "host path: kernel execution");
-  for (auto x : ev)
-    if (x) cudaEventDestroy(x);
-  cudaStreamDestroy(sc);
-  cudaStreamDestroy(sk);
+  if (sc) cudaStreamSynchronize(sc);
+  if (sd) {
+    e = cudaStreamSynchronize(sd);
+    if (e != cudaSuccess && rc == CBP_OK) rc = cuda_fail(e, "host path: copy out");
+  }
+  if (sk) {
+    stats.release(sk);
+    if (img) cudaFreeAsync(img, sk);
+    if (vol) cudaFreeAsync(vol, sk);
+    if (staged) cudaFreeAsync(staged, sk);
+    e = cudaStreamSynchronize(sk);
+    if (e != cudaSuccess && rc == CBP_OK) rc = cuda_fail(e, "host path: kernel execution");
+  }
+  for (auto* v : {&ev_proj, &ev_vol, &ev_done})
+    for (auto x : *v)
+      if (x) cudaEventDestroy(x);
+  for (auto x : {sc, sk, sd})
+    if (x) cudaStreamDestroy(x);
   return rc;
 }
 

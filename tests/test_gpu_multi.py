@@ -58,10 +58,13 @@ def cfg1(torch_cuda):
 
 
 # ------------------------------------------------------------------ host pipeline
-@pytest.mark.parametrize("chunks", [1, 7, 22])
-def test_host_path_angle_chunks_bitwise(cfg1, chunks, monkeypatch):
+@pytest.mark.parametrize("chunks,slabs", [(1, 1), (7, 1), (22, 1), (7, 3), (5, 8)])
+def test_host_path_angle_chunks_bitwise(cfg1, chunks, slabs, monkeypatch):
+    """Angle-chunked uploads with s_begin > 0 launches, and z-slab pipelining (slab k+1
+    uploads / slab k-1 downloads while slab k computes; slabs with k0 > 0, nz_total > nz)."""
     geom, mats, img, ref = cfg1
     monkeypatch.setenv("CBP_HOST_CHUNKS", str(chunks))
+    monkeypatch.setenv("CBP_HOST_SLABS", str(slabs))
     vol = Volume.zeros(256, 256, 256)
     backproject_baseline(ProjectionStack.from_array(img), mats, vol)
     assert sha(vol.data) == ref["baseline"]
