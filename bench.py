@@ -352,7 +352,7 @@ def main() -> None:
 
         launches_per_step = 1 if nw % 4 == 0 else 2
     else:
-        plan = SL.plan_slabs(mats, nh, nw, nx, ny, nz, world, align=32, variant=int(variant))
+        plan = SL.plan_slabs(mats, nh, nw, nx, ny, nz, world, align=16, variant=int(variant))
         backend = SL.CudaBackend(torch)
         k0, k1 = plan.slab(rank)
         vol = backend.empty_slab(plan, k0, k1)

@@ -209,6 +209,32 @@ const void* tiled_kernel_ptr(int variant, bool gen, int c, bool check) {
   return check ? tiled_kernel_ptr_c<true>(variant, gen, c) : tiled_kernel_ptr_c<false>(variant, gen, c);
 }
 
+// half z-run tiles (16 slices), bit-exact, every variant
+template <int V, bool GEN, int C>
+const void* half_fn() {
+  return reinterpret_cast<const void*>(&bp_tiled_half_kernel<V, GEN, kTiles[C].NWX, kTiles[C].NWY, kTiles[C].MINB>);
+}
+template <int V, bool GEN>
+const void* half_by_tile(int c) {
+  switch (c) {
+    case 0: return half_fn<V, GEN, 0>();
+    case 1: return half_fn<V, GEN, 1>();
+    case 3: return half_fn<V, GEN, 3>();
+    case 4: return half_fn<V, GEN, 4>();
+    case 5: return half_fn<V, GEN, 5>();
+    default: return half_fn<V, GEN, 2>();
+  }
+}
+const void* half_kernel_ptr(int variant, bool gen, int c) {
+  switch (variant) {
+    case V_BASELINE: return gen ? half_by_tile<V_BASELINE, true>(c) : half_by_tile<V_BASELINE, false>(c);
+    case V_TRANSPOSE: return gen ? half_by_tile<V_TRANSPOSE, true>(c) : half_by_tile<V_TRANSPOSE, false>(c);
+    case V_SHARE: return half_by_tile<V_SHARE, false>(c);
+    case V_SYMMETRY: return half_by_tile<V_SYMMETRY, false>(c);
+    default: return half_by_tile<V_SUBLINE, false>(c);
+  }
+}
+
 // tolerance mode (CBP_FLAG_FMA_LERP): baseline arithmetic with FMA lerps
 template <bool GEN, int C>
 const void* fmalerp_fn() {
@@ -541,6 +567,20 @@ int launch_staged(StagedCall c, unsigned long long* stats, cudaStream_t st) {
   int rc = validate_staged(c);
   if (rc) return rc;
   if (c.s_begin == c.s_end || samples_nothing(c.nh, c.nw)) return CBP_OK;
+  // a NATURAL slab of 32m + 16 slices: the 32-slice tiles, then the last 16 slices as one layer
+  // of half z-run tiles (fast loops instead of the partial-tile path)
+  constexpr unsigned kHalfExcluded = CBP_FLAG_NAIVE | CBP_FLAG_CHECK | CBP_FLAG_FMA_LERP;
+  if (c.vol_layout == CBP_NATURAL && c.nz > kZR && c.nz % kZR == kZR / 2 && !(c.flags & kHalfExcluded)) {
+    StagedCall head = c, tail = c;
+    head.nz = c.nz - kZR / 2;
+    tail.nz = kZR / 2;
+    tail.k0 = c.k0 + head.nz;
+    tail.vol = c.vol + (size_t)head.nz * (size_t)c.nx * (size_t)c.ny;
+    rc = launch_staged(head, stats, st);
+    return rc ? rc : launch_staged(tail, stats, st);
+  }
+  const bool half = c.nz == kZR / 2 && !(c.flags & kHalfExcluded);
+  const int zr = half ? kZR / 2 : kZR;
   int dev;
   rc = current_device(&dev);
   if (rc) return rc;
@@ -590,7 +630,7 @@ int launch_staged(StagedCall c, unsigned long long* stats, cudaStream_t st) {
   if (!enc) return fail(CBP_ECUDA, "cuTensorMapEncodeTiled unavailable from the driver");
   p.tiles_x = (int)ceil_div(c.nx, plan.TX);
   p.tiles_y = (int)ceil_div(c.ny, plan.TY);
-  p.tiles_z = (int)ceil_div(c.nz, kZR);
+  p.tiles_z = (int)ceil_div(c.nz, zr);
   p.wb = plan.wb;
   p.hb = plan.hb;
   p.stages = plan.stages;
@@ -612,7 +652,8 @@ int launch_staged(StagedCall c, unsigned long long* stats, cudaStream_t st) {
   }
   const void* fn = (c.flags & CBP_FLAG_FMA_LERP)
                        ? (plan.kind == 2 ? fmalerp_by_tile<true>(plan.cfg) : fmalerp_by_tile<false>(plan.cfg))
-                       : tiled_kernel_ptr(key.variant, plan.kind == 2, plan.cfg, (c.flags & CBP_FLAG_CHECK) != 0);
+                   : half ? half_kernel_ptr(key.variant, plan.kind == 2, plan.cfg)
+                          : tiled_kernel_ptr(key.variant, plan.kind == 2, plan.cfg, (c.flags & CBP_FLAG_CHECK) != 0);
   rc = ensure_smem(dev, fn, plan.smem);
   if (rc) return rc;
   const int64_t blocks = (int64_t)p.tiles_x * p.tiles_y * p.tiles_z;
@@ -630,7 +671,7 @@ int launch_staged(StagedCall c, unsigned long long* stats, cudaStream_t st) {
   dim3 g((unsigned)blocks), b(kTileThreads[plan.cfg]);
   void* args[] = {&tmap, &p};
   CK(cudaLaunchKernel(fn, g, b, args, plan.smem, st), "tiled kernel launch");
-  int64_t lp[9] = {plan.TX, plan.TY, kZR, plan.wb, plan.hb, plan.stages, blocks, (int64_t)plan.smem, plan.kind};
+  int64_t lp[9] = {plan.TX, plan.TY, zr, plan.wb, plan.hb, plan.stages, blocks, (int64_t)plan.smem, plan.kind};
   std::memcpy(g_last_plan, lp, sizeof(lp));
   return CBP_OK;
 }

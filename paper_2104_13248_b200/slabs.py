@@ -58,7 +58,7 @@ class SlabPlan:
         return k1 > k0 and self.bands[rank][1] > 0
 
 
-def plan_slabs(mats: np.ndarray, nh: int, nw: int, nx: int, ny: int, nz: int, n_ranks: int, align: int = 32,
+def plan_slabs(mats: np.ndarray, nh: int, nw: int, nx: int, ny: int, nz: int, n_ranks: int, align: int = 16,
                variant: int = 0) -> SlabPlan:
     kb, bands = G.slab_plan(mats, nh, nw, nx, ny, nz, n_ranks, align=align, variant=variant)
     return SlabPlan(tuple(kb), tuple(bands), int(mats.shape[0]), nh, nw, nx, ny, nz, variant)

@@ -113,7 +113,7 @@ def test_loopback_slabs_symmetry_rung_bitwise(torch_cuda, cfg1):
 
     torch = torch_cuda
     geom, mats, img, ref = cfg1
-    plan = slabs.plan_slabs(mats, geom.nh, geom.nw, 256, 256, 256, 4, align=32, variant=int(KernelVariant.SYMMETRY))
+    plan = slabs.plan_slabs(mats, geom.nh, geom.nw, 256, 256, 256, 4, align=16, variant=int(KernelVariant.SYMMETRY))
     vols, _ = run_loopback(torch, torch.from_numpy(img).cuda(), mats, plan, n_chunks=3, transport="ipc")
     full = torch.cat([v for v in vols if v.shape[0] > 0]).cpu().numpy()  # [z][y][x]
     assert sha(full.transpose(2, 1, 0)) == ref["symmetry"]
@@ -149,7 +149,7 @@ def test_backproject_multi_cfg4_n8(torch_cuda):
     n = geom.nx
     img = torch.rand((geom.np, geom.nh, geom.nw), device="cuda", generator=torch.Generator("cuda").manual_seed(4))
     img.mul_(2).sub_(1)
-    plan = slabs.plan_slabs(mats, geom.nh, geom.nw, n, n, n, 8, align=32)
+    plan = slabs.plan_slabs(mats, geom.nh, geom.nw, n, n, n, 8, align=16)
     ref_vol = torch.zeros((n, n, n), device="cuda")
     D.backproject_device(img, mats, ref_vol, geom.np, geom.nh, geom.nw, n, n, n)
     D.sync_status()
@@ -259,3 +259,28 @@ def test_rcp_rn_normal_is_exact_on_its_whole_range(torch_cuda):
         assert bad == 0, hex(first)
     # the footprint's admission bounds sit inside the proven range
     assert np.float32(7.9e-31) >= np.float32(2.0 ** -100) and np.float32(1.2e30) < np.float32(2.0 ** 100)
+
+
+@pytest.mark.parametrize("jitter", [False, True])
+def test_half_zrun_tiles_bitwise(torch_cuda, jitter):
+    """Slabs of 32m + 16 slices run their last 16 slices as a layer of half z-run tiles
+    (bp_tiled_half_kernel); a 16-slice slab runs on it alone.  Fast (circular + u offset)
+    and general (jittered) paths, global slice indices, bitwise vs the C oracle."""
+    from paper_2104_13248_b200 import device as D, geometry as G
+
+    torch = torch_cuda
+    geom = G.build_geometry(nx=100, ny=70, nz=80, nw=151, nh=130, np=61, d=400.0, D=700.0, pixel_pitch_u=1.1,
+                            pixel_pitch_v=0.9, voxel_size=1.3)
+    mats = G.jittered_matrices(geom, 2.0, 5) if jitter else G.u_offset(G.projection_matrices(geom), 7.0)
+    img = uniform(61, 130, 151, 31)
+    vol0 = np.random.default_rng(32).uniform(-1, 1, size=(80, 70, 100)).astype(np.float32)
+    ref = vol0.copy()
+    oracle.baseline(img, mats, ref)
+    staged = D.StagedProjections(torch.from_numpy(img).cuda(), 61, 130, 151)
+    for k0, k1 in [(0, 48), (48, 64), (64, 80), (16, 64)]:
+        v = torch.from_numpy(vol0[k0:k1].copy()).cuda()
+        D.backproject_staged(staged, mats, v, 100, 70, k1 - k0, k0=k0, nz_total=80)
+        st = D.sync_status()
+        assert st["band_violations"] == 0
+        assert v.cpu().numpy().tobytes() == ref[k0:k1].tobytes(), (k0, k1, jitter)
+    assert D.last_plan()["tile_z"] in (16, 32)

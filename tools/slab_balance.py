@@ -47,7 +47,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--ranks", type=int, nargs="+", default=[2, 4, 8])
-    ap.add_argument("--align", type=int, default=32, help="slab boundary granularity in slices (16 or 32)")
+    ap.add_argument("--align", type=int, default=16, help="slab boundary granularity in slices (16 or 32)")
     args = ap.parse_args()
     spec = configs.get_config(args.config)
     geom = spec.geometry()
