@@ -163,7 +163,7 @@ struct TileCfg {
   int NWX, NWY, MINB;
 };
 constexpr int kNumTiles = 6;
-constexpr TileCfg kTiles[kNumTiles] = {{4, 4, 1}, {2, 4, 2}, {2, 2, 3}, {4, 3, 1}, {2, 3, 2}, {4, 5, 1}};
+constexpr TileCfg kTiles[kNumTiles] = {{4, 4, 1}, {2, 4, 2}, {2, 2, 3}, {4, 3, 1}, {2, 3, 2}, {3, 6, 1}};
 
 template <int C>
 using RolesC = WarpRoles<kTiles[C].NWX * kTiles[C].NWY, kTiles[C].MINB>;
