@@ -162,18 +162,20 @@ int get_stats(int dev, cudaStream_t st, unsigned long long** out) {
 struct TileCfg {
   int NWX, NWY, MINB;
 };
-constexpr int kNumTiles = 6;
-constexpr TileCfg kTiles[kNumTiles] = {{4, 4, 1}, {2, 4, 2}, {2, 2, 3}, {4, 3, 1}, {2, 3, 2}, {3, 6, 1}};
+constexpr int kNumTiles = 7;
+constexpr TileCfg kTiles[kNumTiles] = {{4, 4, 1}, {2, 4, 2}, {2, 2, 3}, {4, 3, 1}, {2, 3, 2}, {3, 6, 1}, {2, 2, 4}};
 
 template <int C>
 using RolesC = WarpRoles<kTiles[C].NWX * kTiles[C].NWY, kTiles[C].MINB>;
 constexpr int kTileThreads[kNumTiles] = {RolesC<0>::kThreads, RolesC<1>::kThreads, RolesC<2>::kThreads,
-                                         RolesC<3>::kThreads, RolesC<4>::kThreads, RolesC<5>::kThreads};
+                                         RolesC<3>::kThreads, RolesC<4>::kThreads, RolesC<5>::kThreads,
+                                         RolesC<6>::kThreads};
 // launch register allocation the setmaxnreg split assumes (0: no register reallocation)
 constexpr int kTilePool[kNumTiles] = {
     RolesC<0>::kRealloc ? RolesC<0>::kRegLaunch : 0, RolesC<1>::kRealloc ? RolesC<1>::kRegLaunch : 0,
     RolesC<2>::kRealloc ? RolesC<2>::kRegLaunch : 0, RolesC<3>::kRealloc ? RolesC<3>::kRegLaunch : 0,
-    RolesC<4>::kRealloc ? RolesC<4>::kRegLaunch : 0, RolesC<5>::kRealloc ? RolesC<5>::kRegLaunch : 0};
+    RolesC<4>::kRealloc ? RolesC<4>::kRegLaunch : 0, RolesC<5>::kRealloc ? RolesC<5>::kRegLaunch : 0,
+    RolesC<6>::kRealloc ? RolesC<6>::kRegLaunch : 0};
 
 template <int V, bool GEN, int C, bool CHECK>
 const void* tiled_fn() {
@@ -189,6 +191,7 @@ const void* tiled_by_tile(int c) {
     case 3: return tiled_fn<V, GEN, 3, CHECK>();
     case 4: return tiled_fn<V, GEN, 4, CHECK>();
     case 5: return tiled_fn<V, GEN, 5, CHECK>();
+    case 6: return tiled_fn<V, GEN, 6, CHECK>();
     default: return tiled_fn<V, GEN, 2, CHECK>();
   }
 }
@@ -222,6 +225,7 @@ const void* half_by_tile(int c) {
     case 3: return half_fn<V, GEN, 3>();
     case 4: return half_fn<V, GEN, 4>();
     case 5: return half_fn<V, GEN, 5>();
+    case 6: return half_fn<V, GEN, 6>();
     default: return half_fn<V, GEN, 2>();
   }
 }
@@ -249,6 +253,7 @@ const void* fmalerp_by_tile(int c) {
     case 3: return fmalerp_fn<GEN, 3>();
     case 4: return fmalerp_fn<GEN, 4>();
     case 5: return fmalerp_fn<GEN, 5>();
+    case 6: return fmalerp_fn<GEN, 6>();
     default: return fmalerp_fn<GEN, 2>();
   }
 }
@@ -668,8 +673,35 @@ int launch_staged(StagedCall c, unsigned long long* stats, cudaStream_t st) {
       return fail(CBP_ECUDA, buf);
     }
   }
-  dim3 g((unsigned)blocks), b(kTileThreads[plan.cfg]);
-  void* args[] = {&tmap, &p};
+  // angle-independent r1[2] * fkk table (see TyTab): every matrix of the launch shares m[6]
+  static thread_local TyTab tytab;
+  p.ty_const = c.nz <= kTyTabMax ? 1 : 0;
+  // the same loop forms texel byte addresses with one subnormal FMA (bp_kernels.cuh, ADDR_W4):
+  // exact while |box base - v0 * row pitch| < 2^24
+  if (c.nh * (int64_t)plan.wb * 4 >= (1 << 24) - (1 << 19)) p.ty_const = 0;
+  {
+    uint32_t m6_bits;
+    std::memcpy(&m6_bits, c.mats_host + 12 * c.s_begin + 6, 4);
+    for (int64_t s = c.s_begin; s < c.s_end && p.ty_const; ++s) {
+      uint32_t b;
+      std::memcpy(&b, c.mats_host + 12 * s + 6, 4);
+      if (b != m6_bits) p.ty_const = 0;
+    }
+    if (p.ty_const) {
+      const float m6 = c.mats_host[12 * c.s_begin + 6];
+      const int64_t nzh = c.nz_total >> 1;
+      const int64_t n_tab = std::min<int64_t>(kTyTabMax, ceil_div(c.nz, kZR) * kZR);
+      for (int64_t q = 0; q < n_tab; ++q) {
+        const int64_t kg = c.k0 + q;
+        const int64_t kk = (v_mirror(key.variant) && kg >= nzh) ? c.nz_total - 1 - kg : kg;
+        const volatile float prod = m6 * (float)kk;  // one rounded float32 product, as the kernel's __fmul_rn
+        tytab.v[q] = prod;
+      }
+    }
+  }
+  if (p.tiles_z > 65535) return fail(CBP_EINVAL, "volume too deep for one launch");
+  dim3 g((unsigned)(p.tiles_x * p.tiles_y), (unsigned)p.tiles_z), b(kTileThreads[plan.cfg]);
+  void* args[] = {&tmap, &p, &tytab};
   CK(cudaLaunchKernel(fn, g, b, args, plan.smem, st), "tiled kernel launch");
   int64_t lp[9] = {plan.TX, plan.TY, zr, plan.wb, plan.hb, plan.stages, blocks, (int64_t)plan.smem, plan.kind};
   std::memcpy(g_last_plan, lp, sizeof(lp));

@@ -282,7 +282,7 @@ def test_band_violation_is_reported(torch_cuda):
         D.sync_status()
 
 
-@pytest.mark.parametrize("tile_cfg", range(6))
+@pytest.mark.parametrize("tile_cfg", range(7))
 def test_every_tile_shape_bitwise(torch_cuda, tile_cfg):
     """Every tile shape the planner can pick (one or two CTAs per SM, 8..20 consumer
     warps) reproduces the reference's config-1 bits, and the general (tilted-matrix)
