@@ -183,6 +183,7 @@ const void* tiled_fn() {
       &bp_tiled_kernel<V, GEN, kTiles[C].NWX, kTiles[C].NWY, kTiles[C].MINB, CHECK>);
 }
 
+#if !CBP_DEV_SLIM
 template <int V, bool GEN, bool CHECK>
 const void* tiled_by_tile(int c) {
   switch (c) {
@@ -208,9 +209,16 @@ const void* tiled_kernel_ptr_c(int variant, bool gen, int c) {
   }
 }
 
+#endif
 const void* tiled_kernel_ptr(int variant, bool gen, int c, bool check) {
+#if CBP_DEV_SLIM  // kernel-tuning builds: only the baseline fast-path instances of tile shapes 0 and 1 (seconds to compile)
+  (void)variant; (void)gen; (void)check;
+  return c == 1 ? tiled_fn<V_BASELINE, false, 1, false>() : c == 3 ? tiled_fn<V_BASELINE, false, 3, false>() : tiled_fn<V_BASELINE, false, 0, false>();
+#else
   return check ? tiled_kernel_ptr_c<true>(variant, gen, c) : tiled_kernel_ptr_c<false>(variant, gen, c);
+#endif
 }
+#if !CBP_DEV_SLIM
 
 // half z-run tiles (16 slices), bit-exact, every variant
 template <int V, bool GEN, int C>
@@ -229,7 +237,11 @@ const void* half_by_tile(int c) {
     default: return half_fn<V, GEN, 2>();
   }
 }
+#endif
 const void* half_kernel_ptr(int variant, bool gen, int c) {
+#if CBP_DEV_SLIM
+  return tiled_kernel_ptr(variant, gen, c, false);
+#else
   switch (variant) {
     case V_BASELINE: return gen ? half_by_tile<V_BASELINE, true>(c) : half_by_tile<V_BASELINE, false>(c);
     case V_TRANSPOSE: return gen ? half_by_tile<V_TRANSPOSE, true>(c) : half_by_tile<V_TRANSPOSE, false>(c);
@@ -237,8 +249,10 @@ const void* half_kernel_ptr(int variant, bool gen, int c) {
     case V_SYMMETRY: return half_by_tile<V_SYMMETRY, false>(c);
     default: return half_by_tile<V_SUBLINE, false>(c);
   }
+#endif
 }
 
+#if !CBP_DEV_SLIM
 // tolerance mode (CBP_FLAG_FMA_LERP): baseline arithmetic with FMA lerps
 template <bool GEN, int C>
 const void* fmalerp_fn() {
@@ -258,6 +272,7 @@ const void* fmalerp_by_tile(int c) {
   }
 }
 
+#endif
 const void* naive_kernel_ptr(int variant) {
   switch (variant) {
     case V_BASELINE: return reinterpret_cast<const void*>(&bp_naive_kernel<V_BASELINE>);
@@ -602,7 +617,7 @@ int launch_staged(StagedCall c, unsigned long long* stats, cudaStream_t st) {
   rc = get_plan(key, c.mats_host, st, &plan);
   if (rc) return rc;
 
-  BPParams p;
+  BPParams p{};
   std::memset(&p, 0, sizeof(p));
   p.proj = c.staged;
   p.mats = plan.mats_dev();
@@ -655,10 +670,15 @@ int launch_staged(StagedCall c, unsigned long long* stats, cudaStream_t st) {
                   plan.hb, (long long)c.pitch);
     return fail(CBP_ECUDA, buf);
   }
-  const void* fn = (c.flags & CBP_FLAG_FMA_LERP)
+  const void* fn =
+#if CBP_DEV_SLIM
+      tiled_kernel_ptr(key.variant, false, plan.cfg, false);
+#else
+      (c.flags & CBP_FLAG_FMA_LERP)
                        ? (plan.kind == 2 ? fmalerp_by_tile<true>(plan.cfg) : fmalerp_by_tile<false>(plan.cfg))
                    : half ? half_kernel_ptr(key.variant, plan.kind == 2, plan.cfg)
                           : tiled_kernel_ptr(key.variant, plan.kind == 2, plan.cfg, (c.flags & CBP_FLAG_CHECK) != 0);
+#endif
   rc = ensure_smem(dev, fn, plan.smem);
   if (rc) return rc;
   const int64_t blocks = (int64_t)p.tiles_x * p.tiles_y * p.tiles_z;

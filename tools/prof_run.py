@@ -16,6 +16,7 @@ ap.add_argument("--variant", default="baseline")
 ap.add_argument("--flags", type=int, default=0)
 ap.add_argument("--uniform", action="store_true", help="uniform inputs instead of the phantom (faster setup)")
 ap.add_argument("--slab", default=None, help="k0:k1 -- back-project only this z-slab (global indices; for ncu on cfg4)")
+ap.add_argument("--sha", action="store_true", help="print the sha256 of the resulting slab (A/B bit-equality checks)")
 a = ap.parse_args()
 spec = configs.get_config(a.config)
 geom = spec.geometry()
@@ -37,3 +38,6 @@ torch.cuda.synchronize()
 ms = [ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(a.iters)]
 print("plan", D.last_plan(), "stats", D.sync_status())
 print("ms", [round(x, 3) for x in ms], "GUPS", [round(geom.nx * geom.ny * (k1 - k0) * geom.np / (x * 1e6), 1) for x in ms])
+if a.sha:
+    import hashlib
+    print("sha", hashlib.sha256(vol.cpu().numpy().tobytes()).hexdigest())
