@@ -62,18 +62,28 @@ def test_device_entry_points_fail_loudly_without_gpu():
 
 def test_no_fma_contraction_in_backprojection_sass():
     """Bit-exactness needs separately rounded products and sums: the SASS of the
-    back-projection kernels must contain no fused FFMA2 (the only FFMA allowed are the
-    explicit Newton steps inside __frcp_rn)."""
+    back-projection kernels must contain no fused multiply-add on sample values.  The only
+    FFMA2 allowed is the texel ADDRESS of the guard-free loop (floor(y) * row pitch + base on
+    subnormal floats, exact by construction: bp_kernels.cuh hot_loop): one per slice pair,
+    recognisable by its broadcast scalar operands: row pitch as multiplier and, above all, the
+    base address as ADDEND -- every sum of the sample arithmetic adds a packed pair.  (Scalar
+    FFMA are the explicit Newton steps of the correctly rounded reciprocal.)"""
     out = subprocess.run(["cuobjdump", "-sass", str(_lib.LIB_PATH)], capture_output=True, text=True)
     if out.returncode != 0:
         pytest.skip("cuobjdump unavailable")
     funcs = re.split(r"\n\s+Function : ", out.stdout)
-    checked = 0
+    addr_fma = re.compile(r"FFMA2 R\d+, R\d+(\.reuse)?\.F32x2\.LO_HI, U?R\d+(\.reuse)?\.F32, R\d+(\.reuse)?\.F32 ;")
+    checked = with_addr = 0
     for f in funcs:
         name = f.split("\n", 1)[0]
-        if "bp_tiled_kernel" in name or "bp_naive_kernel" in name:
+        if "bp_tiled_kernel" in name or "bp_naive_kernel" in name or "bp_tiled_half_kernel" in name:
             checked += 1
-            assert "FFMA2" not in f, name
+            fused = [ln for ln in f.split("\n") if "FFMA2" in ln]
+            assert all(addr_fma.search(ln) for ln in fused), (name, [ln for ln in fused if not addr_fma.search(ln)][:3])
+            # one guard-free loop per kernel at most: 16 slice pairs (8 in the half z-run kernels)
+            assert len(fused) in (0, 8, 16), (name, len(fused))
+            with_addr += bool(fused)
         if "bp_tiled_fmalerp_kernel" in name:  # the opt-in tolerance mode does fuse its lerps
             assert "FFMA2" in f, name
+    assert with_addr > 0
     assert checked > 0

@@ -21,6 +21,7 @@ a = ap.parse_args()
 spec = configs.get_config(a.config)
 geom = spec.geometry()
 mats = spec.matrices(geom)
+torch.manual_seed(11)
 if a.uniform:
     img = torch.rand((geom.np, geom.nh, geom.nw), device="cuda") * 2 - 1
 else:
