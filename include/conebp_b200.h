@@ -200,8 +200,9 @@ int cbp_forward_project_f32(const float* vol_dev, int64_t nx, int64_t ny, int64_
  * cosine weighting D/sqrt(D^2 + ((u-cu)pu)^2 + ((v-cv)pv)^2) and row-wise spatial
  * Ram-Lak filtering (tau = detector pitch scaled to the isocentre) of NATURAL raw
  * projections [np][nh][nw] on the device, written into the staging layout
- * [np][nh][pitch] that cbp_backproject_staged reads.  Zero-padded FFT convolution
- * (cuFFT), float32.  Stream-ordered.
+ * [np][nh][pitch] that cbp_backproject_staged reads.  Zero-padded FFT convolution in one
+ * fused kernel (shared-memory radix-8 transform, two rows per complex transform: each row is
+ * read once and written once), float32, nw <= 4096.  Stream-ordered.
  */
 int cbp_fdk_filter_f32(const float* raw_dev, int64_t np, int64_t nh, int64_t nw, double D,
                        double pixel_pitch_u, double pixel_pitch_v, double cu, double cv,

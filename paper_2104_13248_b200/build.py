@@ -38,7 +38,6 @@ NVCC_FLAGS = [
     "-shared",
     "-cudart",
     "static",
-    "-lcufft",
     "-Xlinker",
     "-rpath,/usr/local/cuda/lib64",
 ]

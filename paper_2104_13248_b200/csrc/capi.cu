@@ -1278,12 +1278,95 @@ int cbp_forward_project_f32(const float* vol_dev, int64_t nx, int64_t ny, int64_
   fp.np = (int)np; fp.nh = (int)nh; fp.nw = (int)nw; fp.nx = (int)nx; fp.ny = (int)ny; fp.nz = (int)nz;
   fp.pu = pixel_pitch_u; fp.pv = pixel_pitch_v; fp.cu = cu; fp.cv = cv; fp.s = voxel_size;
   const int64_t rays = np * nh * nw;
-  bp_forward_kernel<<<(unsigned)ceil_div(rays, 256), 256, 0, st>>>(fp);
+  int s_exp = 0;
+  const bool pow2 = std::frexp(fp.s, &s_exp) == 0.5 && s_exp > -500 && s_exp < 500;  // 1/s exact, no over/underflow
+  if (pow2)
+    bp_forward_kernel<true><<<(unsigned)ceil_div(rays, 256), 256, 0, st>>>(fp);
+  else
+    bp_forward_kernel<false><<<(unsigned)ceil_div(rays, 256), 256, 0, st>>>(fp);
   cudaError_t e = cudaGetLastError();
   cudaFreeAsync(vd, st);
   if (e != cudaSuccess) return cuda_fail(e, "forward kernel launch");
   return CBP_OK;
 }
+
+}  // extern "C"
+
+namespace {
+// host tables of the fused FDK filter for one (N, tau): N-th roots of unity and the Ram-Lak
+// spectrum in the digit-reversed order the forward passes leave it in (fdk.cuh)
+struct FdkTables {
+  std::vector<float> tw;  // N x (re, im)
+  std::vector<float> hp;  // N
+};
+void fdk_position_frequencies(int base, int len, int c, int stride, const int* radix, std::vector<int>& freq) {
+  if (len == 1) {
+    freq[base] = c;
+    return;
+  }
+  const int r = *radix, sub = len / r;
+  for (int q = 0; q < r; ++q) fdk_position_frequencies(base + q * sub, sub, c + stride * q, stride * r, radix + 1, freq);
+}
+std::shared_ptr<const FdkTables> fdk_tables(int logn, double tau) {
+  static std::mutex mu;
+  static std::map<std::pair<int, double>, std::shared_ptr<const FdkTables>> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find({logn, tau});
+  if (it != cache.end()) return it->second;
+  if (cache.size() >= 8) cache.clear();
+  const int N = 1 << logn;
+  const double pi = 3.14159265358979323846;
+  auto tp = std::make_shared<FdkTables>();
+  FdkTables& t = *tp;
+  t.tw.resize(2 * (size_t)N);
+  std::vector<double> cosN(N);
+  for (int k = 0; k < N; ++k) {
+    cosN[k] = std::cos(2.0 * pi * (double)k / N);
+    t.tw[2 * k] = (float)cosN[k];
+    t.tw[2 * k + 1] = (float)(-std::sin(2.0 * pi * (double)k / N));
+  }
+  // exact DFT of the zero-padded spatial Ram-Lak kernel (real, even), times tau / N
+  std::vector<double> H(N / 2 + 1);
+  for (int k = 0; k <= N / 2; ++k) {
+    double acc = 1.0 / (4.0 * tau * tau);
+    for (int n = 1; n < N / 2; n += 2)
+      acc += 2.0 * (-1.0 / (pi * pi * (double)n * n * tau * tau)) * cosN[(size_t)((long long)k * n % N)];
+    H[k] = acc * tau / N;
+  }
+  int radix[16];
+  const int A = fdk_radix8_passes(logn);
+  for (int i = 0; i < A; ++i) radix[i] = 8;
+  radix[A] = 1 << (logn - 3 * A);
+  std::vector<int> freq(N);
+  fdk_position_frequencies(0, N, 0, 1, radix, freq);
+  t.hp.resize(N);
+  for (int p = 0; p < N; ++p) {
+    const int k = freq[p];
+    t.hp[p] = (float)H[k <= N / 2 ? k : N - k];
+  }
+  cache[{logn, tau}] = tp;
+  return tp;
+}
+
+template <int LOGN>
+cudaError_t fdk_launch(const float* raw, const float* wtab, const float2* tw, const float* hp, int nh, int nw, int pitch,
+                       long long rows, float* out, int sms, cudaStream_t st) {
+  constexpr int N = 1 << LOGN;
+  const size_t smem = (size_t)(N + N / 16 + 1) * sizeof(float2);
+  const int threads = std::max(32, std::min(256, N / 8));
+  cudaError_t e = cudaSuccess;
+  if (smem > 48 * 1024)
+    e = cudaFuncSetAttribute(fdk_filter_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const long long pairs = (rows + 1) / 2;
+  const long long per_sm = std::max<long long>(1, std::min<long long>(2048 / threads, (200 * 1024) / (long long)smem));
+  const unsigned grid = (unsigned)std::min<long long>(pairs, per_sm * sms);
+  fdk_filter_kernel<LOGN><<<grid, threads, smem, st>>>(raw, wtab, tw, hp, nh, nw, pitch, rows, out);
+  return cudaGetLastError();
+}
+}  // namespace
+
+extern "C" {
 
 int cbp_fdk_filter_f32(const float* raw_dev, int64_t np, int64_t nh, int64_t nw, double D, double pixel_pitch_u,
                        double pixel_pitch_v, double cu, double cv, double tau, float* out_dev, int64_t pitch,
@@ -1291,73 +1374,44 @@ int cbp_fdk_filter_f32(const float* raw_dev, int64_t np, int64_t nh, int64_t nw,
   if (!raw_dev || !out_dev) return fail(CBP_EINVAL, "null buffer");
   if (np < 1 || nh < 1 || nw < 2 || pitch < nw || (pitch & 3) || !(D > 0) || !(tau > 0))
     return fail(CBP_EINVAL, "invalid FDK filter arguments");
+  if (nw > 4096) return fail(CBP_EINVAL, "FDK filter: detector rows longer than 4096 pixels are not supported");
   int dev;
   int rc = current_device(&dev);
   if (rc) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
-  int nfft = 1;
-  while (nfft < 2 * nw) nfft <<= 1;
-  const int nspec = nfft / 2 + 1;
-  // exact DFT of the zero-padded spatial Ram-Lak kernel (even, real), times tau / nfft
-  std::vector<float> Hh(nspec);
-  {
-    const double pi = 3.14159265358979323846;
-    for (int k = 0; k < nspec; ++k) {
-      double acc = 1.0 / (4.0 * tau * tau);
-      for (int n = 1; n < nfft / 2; n += 2)
-        acc += 2.0 * (-1.0 / (pi * pi * (double)n * n * tau * tau)) * std::cos(2.0 * pi * (double)k * n / nfft);
-      Hh[k] = (float)(acc * tau / nfft);
+  int logn = 2;
+  while ((1ll << logn) < 2 * nw) ++logn;
+  const int N = 1 << logn;
+  const std::shared_ptr<const FdkTables> tabp = fdk_tables(logn, tau);
+  const FdkTables& tab = *tabp;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  float *tw = nullptr, *hp = nullptr, *wtab = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&tw), 2 * (size_t)N * sizeof(float), st);
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&hp), (size_t)N * sizeof(float), st);
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&wtab), (size_t)nh * nw * sizeof(float), st);
+  // pageable sources: the copies are staged before the calls return, the cache may change afterwards
+  if (e == cudaSuccess) e = cudaMemcpyAsync(tw, tab.tw.data(), 2 * (size_t)N * sizeof(float), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(hp, tab.hp.data(), (size_t)N * sizeof(float), cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) rc = cuda_fail(e, "FDK filter: tables");
+  if (rc == CBP_OK) {
+    dim3 b(128), g((unsigned)ceil_div(nw, 128), (unsigned)nh);
+    fdk_weight_table_kernel<<<g, b, 0, st>>>((int)nh, (int)nw, D, pixel_pitch_u, pixel_pitch_v, cu, cv, wtab);
+    const long long rows = (long long)np * nh;
+    const float2* tw2 = reinterpret_cast<const float2*>(tw);
+    switch (logn) {
+#define CBP_FDK_CASE(L) \
+  case L: e = fdk_launch<L>(raw_dev, wtab, tw2, hp, (int)nh, (int)nw, (int)pitch, rows, out_dev, sms, st); break;
+      CBP_FDK_CASE(2) CBP_FDK_CASE(3) CBP_FDK_CASE(4) CBP_FDK_CASE(5) CBP_FDK_CASE(6) CBP_FDK_CASE(7)
+      CBP_FDK_CASE(8) CBP_FDK_CASE(9) CBP_FDK_CASE(10) CBP_FDK_CASE(11) CBP_FDK_CASE(12) CBP_FDK_CASE(13)
+#undef CBP_FDK_CASE
+      default: e = cudaErrorInvalidValue;
     }
-  }
-  const long long rows_total = (long long)np * nh;
-  const long long chunk = std::max<long long>(1, std::min<long long>(rows_total, (256ll << 20) / (8ll * nfft)));
-  float *H = nullptr, *buf = nullptr;
-  cufftComplex* spec = nullptr;
-  cufftHandle fwd = 0, inv = 0;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&H), nspec * sizeof(float), st);
-  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&buf), (size_t)chunk * nfft * sizeof(float), st);
-  if (e == cudaSuccess)
-    e = cudaMallocAsync(reinterpret_cast<void**>(&spec), (size_t)chunk * nspec * sizeof(cufftComplex), st);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(H, Hh.data(), nspec * sizeof(float), cudaMemcpyHostToDevice, st);
-  if (e != cudaSuccess) rc = cuda_fail(e, "FDK filter: allocation");
-  for (long long r0 = 0; r0 < rows_total && rc == CBP_OK; r0 += chunk) {
-    const long long rows = std::min(chunk, rows_total - r0);
-    if (!fwd || rows != chunk) {  // plans for this batch size
-      if (fwd) cufftDestroy(fwd);
-      if (inv) cufftDestroy(inv);
-      fwd = inv = 0;
-      int n[1] = {nfft};
-      if (cufftPlanMany(&fwd, 1, n, nullptr, 1, nfft, nullptr, 1, nspec, CUFFT_R2C, (int)rows) != CUFFT_SUCCESS ||
-          cufftPlanMany(&inv, 1, n, nullptr, 1, nspec, nullptr, 1, nfft, CUFFT_C2R, (int)rows) != CUFFT_SUCCESS ||
-          cufftSetStream(fwd, st) != CUFFT_SUCCESS || cufftSetStream(inv, st) != CUFFT_SUCCESS) {
-        rc = fail(CBP_ECUDA, "FDK filter: cuFFT plan creation failed");
-        break;
-      }
-    }
-    const int gz = 1024;
-    dim3 b(256), g((unsigned)std::min<long long>(ceil_div(nfft, 256), 16), (unsigned)ceil_div(rows, gz), gz);
-    fdk_weight_pad_kernel<<<g, b, 0, st>>>(raw_dev + r0 * nw, (int)nh, (int)nw, nfft, rows, r0, D, pixel_pitch_u,
-                                           pixel_pitch_v, cu, cv, buf);
-    if (cufftExecR2C(fwd, buf, spec) != CUFFT_SUCCESS) {
-      rc = fail(CBP_ECUDA, "FDK filter: cufftExecR2C failed");
-      break;
-    }
-    const long long ns = rows * nspec;
-    fdk_spectrum_kernel<<<(unsigned)ceil_div(ns, 256), 256, 0, st>>>(spec, H, nspec, rows);
-    if (cufftExecC2R(inv, spec, buf) != CUFFT_SUCCESS) {
-      rc = fail(CBP_ECUDA, "FDK filter: cufftExecC2R failed");
-      break;
-    }
-    dim3 g2((unsigned)std::min<long long>(ceil_div(pitch, 256), 16), (unsigned)ceil_div(rows, gz), gz);
-    fdk_crop_kernel<<<g2, b, 0, st>>>(buf, nfft, (int)nw, (int)pitch, rows, out_dev + r0 * pitch);
-    e = cudaGetLastError();
     if (e != cudaSuccess) rc = cuda_fail(e, "FDK filter: kernel launch");
   }
-  if (fwd) cufftDestroy(fwd);
-  if (inv) cufftDestroy(inv);
-  if (H) cudaFreeAsync(H, st);
-  if (buf) cudaFreeAsync(buf, st);
-  if (spec) cudaFreeAsync(spec, st);
+  if (tw) cudaFreeAsync(tw, st);
+  if (hp) cudaFreeAsync(hp, st);
+  if (wtab) cudaFreeAsync(wtab, st);
   return rc;
 }
 

@@ -8,8 +8,9 @@ device, written straight into the back-projector's staging layout:
   spatial Ram-Lak filter (tau = pixel pitch scaled to the isocentre), exactly the
   definition of :func:`paper_2104_13248_b200.phantom.cosine_weight` /
   :func:`~paper_2104_13248_b200.phantom.ramp_filter`, computed by
-  ``cbp_fdk_filter_f32`` (weight/pad kernel, cuFFT R2C, exact Ram-Lak spectrum,
-  cuFFT C2R, crop into the staging layout);
+  ``cbp_fdk_filter_f32`` (one fused kernel: weight, zero-padded shared-memory FFT of
+  two rows per complex transform, exact Ram-Lak spectrum, inverse, crop into the
+  staging layout -- each row read once and written once);
 * ``fdk_reconstruct`` -- filter, back-project (reference BASELINE arithmetic), scale
   by ``pi * d^2 / np`` (dbeta/2 with the reference's 1/z^2 weight, z = d at the
   isocentre) for a full 360-degree orbit.

@@ -175,6 +175,16 @@ def forward_cases():
     t2 = rasterize_phantom(ph, (16, 14, 10), 1.0)
     out["odd_truth"] = t2.data
     out["odd_proj"] = forward_project(t2, g2).data
+    # voxel sizes other than 1: a power of two (the projector multiplies by the exact reciprocal)
+    # and 0.7 (it divides, like the reference)
+    for tag, vs in (("half", 0.5), ("p7", 0.7)):
+        g3 = build_geometry(nx=10, ny=12, nz=9, nw=30, nh=22, np=5, d=20.0, D=33.0, voxel_size=vs,
+                            pixel_pitch_u=0.6, pixel_pitch_v=0.55)
+        rng = np.random.default_rng(17)
+        from conebp import Volume
+        t3 = Volume.from_array(rng.uniform(0.0, 1.0, (9, 12, 10)).astype(np.float32))
+        out[f"{tag}_truth"] = t3.data
+        out[f"{tag}_proj"] = forward_project(t3, g3).data
     np.savez_compressed(HERE / "forward.npz", **out)
     print("forward:", sorted(out), flush=True)
 

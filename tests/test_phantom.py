@@ -52,6 +52,12 @@ def test_forward_projector_bitwise():
     assert p1.data.tobytes() == g["tiny_proj"].tobytes()
     p2 = P.forward_project(Volume.from_array(g["odd_truth"]), odd_geom())
     assert p2.data.tobytes() == g["odd_proj"].tobytes()
+    # voxel sizes other than 1: 0.5 (multiplication by the exact reciprocal) and 0.7 (division)
+    for tag, vs in (("half", 0.5), ("p7", 0.7)):
+        g3 = G.build_geometry(nx=10, ny=12, nz=9, nw=30, nh=22, np=5, d=20.0, D=33.0, voxel_size=vs,
+                              pixel_pitch_u=0.6, pixel_pitch_v=0.55)
+        p3 = P.forward_project(Volume.from_array(g[f"{tag}_truth"]), g3)
+        assert p3.data.tobytes() == g[f"{tag}_proj"].tobytes(), tag
 
 
 @pytest.mark.gpu

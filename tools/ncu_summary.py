@@ -51,7 +51,7 @@ for label, k in keys:
     v, u = g(k)
     print(f"| {label} (`{k}`) | {v} {u} |")
 inst = g("smsp__inst_executed.sum")[0]
-SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 try:
     dram = sum(float(g(k)[0]) * SCALE.get(g(k)[1], 1) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
     print(f"| DRAM traffic per launch (read + write) | {dram / 1e6:.1f} MB |")

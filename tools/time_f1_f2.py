@@ -2,10 +2,10 @@
 
     python tools/time_f1_f2.py [--configs 1 3]
 
-f1 ``cbp_fdk_filter_f32``: cosine weight + zero-pad kernel, cuFFT R2C, Ram-Lak spectrum
-multiply, cuFFT C2R, crop into the staging layout.  Reported against HBM: compulsory bytes
-= raw read + staged write (8 B per texel); "pass bytes" adds the round trips through the
-zero-padded rows and the complex spectrum that the five-launch pipeline makes.
+f1 ``cbp_fdk_filter_f32``: one fused kernel (weight, zero-padded shared-memory FFT of two rows
+per complex transform, Ram-Lak spectrum, inverse, crop into the staging layout).  Reported
+against HBM on its compulsory bytes = raw read + staged write (8 B per texel), which is all it
+moves, and as FP32 work (10 N log2 N flops per complex transform pair forward + inverse).
 f2 ``cbp_forward_project_f32`` (float64 ray marching, the reference's arithmetic): rays/s
 on the config's grid (a subset of 32 angles).
 """
@@ -44,6 +44,7 @@ def timed(fn, iters=3):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", type=int, nargs="+", default=[1, 3])
+    ap.add_argument("--skip-f2", action="store_true")
     args = ap.parse_args()
     peaks = json.loads((Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").read_text()) \
         if (Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").exists() else {"hbm_gbs": 6650.0}
@@ -69,18 +70,18 @@ def main():
         while nfft < 2 * nw:
             nfft *= 2
         comp = 8.0 * texels
-        passes = 4.0 * texels + 4.0 * n_proj * nh * nfft * 2 + 8.0 * n_proj * nh * (nfft // 2 + 1) * 2 \
-            + 4.0 * n_proj * nh * nfft * 2 + 4.0 * texels  # weight+pad, R2C r/w, multiply r/w, C2R r/w, crop
+        logn = nfft.bit_length() - 1
+        flops = 10.0 * nfft * logn * (n_proj * nh / 2.0)
         r1 = {"ms": ms1, "texels_per_s": texels / ms1 / 1e-3, "compulsory_gbs": comp / ms1 / 1e6,
-              "pass_bytes_gbs": passes / ms1 / 1e6, "hbm_peak_gbs": peaks.get("hbm_gbs"),
-              "compulsory_frac": comp / ms1 / 1e6 / peaks.get("hbm_gbs", 6650.0)}
+              "hbm_peak_gbs": peaks.get("hbm_gbs"), "compulsory_frac": comp / ms1 / 1e6 / peaks.get("hbm_gbs", 6650.0),
+              "transform_length": nfft, "fft_tflops": flops / ms1 / 1e9}
         del raw, staged
         # f2 on the config's grid (bounded: cfg3 is 1024^3 x 1440 x 1536^2 rays -> time a subset of angles)
         n_sub = min(n_proj, 32)
         vol = torch.rand((geom.nz, geom.ny, geom.nx), device="cuda")
         views = _views_array(circular_views(geom)[:n_sub])
         r2 = None
-        if True:
+        if not args.skip_f2:
             outp = torch.empty((n_sub, nh, nw), device="cuda")
 
             def f2():
