@@ -872,9 +872,13 @@ int cbp_backproject_host_f32(const float* img_host, int64_t np, int64_t nh, int6
   // the upload stream while the compute stream stages and back-projects the chunks already
   // resident (each launch accumulates angles [s0, s1) in ascending order: bitwise identical
   // to one launch).  A NATURAL volume is also split into z-slabs (contiguous, cut on the
-  // kernel's 32-slice z-runs): slab 0 is uploaded first, slab k+1 uploads while slab k
-  // computes and slab k downloads on the third stream while slab k+1 computes, so only
-  // the projection upload of slab 0 and the last slab's download are not hidden.
+  // kernel's 32-slice z-runs): the first slab is uploaded first, the next one uploads while
+  // one computes and each downloads on the third stream while its successor computes, so
+  // only the first slab's upload, the first projection chunk and the last download are not
+  // hidden.  The first slab is the CENTRAL one: it is the most expensive (every angle samples
+  // it), so its chunked launches keep the SMs busy for as long as the projections take to
+  // arrive (cfg4: 0.85 s of compute against 0.63 s of upload; a cheap end slab left the GPU
+  // idle for most of the upload).
   const size_t per_proj = (size_t)nh * nw, ib = (size_t)np * per_proj * 4, vb = (size_t)nx * ny * nz * 4;
   const bool direct = img_layout == CBP_NATURAL && (nw & 3) == 0;  // natural layout is the staging layout
   const int64_t pitch = cbp_staged_pitch(nw);
@@ -889,6 +893,15 @@ int cbp_backproject_host_f32(const float* img_host, int64_t np, int64_t nh, int6
   std::vector<int64_t> zb((size_t)n_slabs + 1);
   for (int64_t k = 0; k <= n_slabs; ++k) zb[k] = (k == n_slabs) ? nz : (nz * k / n_slabs) / kZR * kZR;
   const size_t slice = (size_t)nx * ny;
+  std::vector<int64_t> order;  // processing order of the slabs: centre first, then outwards
+  {
+    const int64_t c = n_slabs / 2;
+    order.push_back(c);
+    for (int64_t d = 1; d < n_slabs; ++d) {
+      if (c + d < n_slabs) order.push_back(c + d);
+      if (c - d >= 0) order.push_back(c - d);
+    }
+  }
 
   cudaStream_t sc = nullptr, sk = nullptr, sd = nullptr;
   std::vector<cudaEvent_t> ev_proj((size_t)n_chunks, nullptr), ev_vol((size_t)n_slabs, nullptr),
@@ -909,13 +922,13 @@ int cbp_backproject_host_f32(const float* img_host, int64_t np, int64_t nh, int6
   if (e == cudaSuccess) e = cudaStreamSynchronize(sk);  // allocations visible to the copy streams
   if (e != cudaSuccess) rc = cuda_fail(e, "host path: streams / allocation");
   if (rc == CBP_OK) rc = stats.alloc(sk);
-  // uploads, in the order they are needed: slab 0, the projection chunks, the other slabs
+  // uploads, in the order they are needed: the first slab, the projection chunks, the other slabs
   auto up_slab = [&](int64_t k) {
     const size_t off = (size_t)zb[k] * slice, n = (size_t)(zb[k + 1] - zb[k]) * slice;
     cudaError_t r = cudaMemcpyAsync(vol + off, vol_host + off, n * 4, cudaMemcpyHostToDevice, sc);
     return r == cudaSuccess ? cudaEventRecord(ev_vol[k], sc) : r;
   };
-  if (rc == CBP_OK && (e = up_slab(0)) != cudaSuccess) rc = cuda_fail(e, "host path: volume upload");
+  if (rc == CBP_OK && (e = up_slab(order[0])) != cudaSuccess) rc = cuda_fail(e, "host path: volume upload");
   for (int64_t q = 0; q < n_chunks && rc == CBP_OK; ++q) {
     const int64_t s0 = np * q / n_chunks, s1 = np * (q + 1) / n_chunks;
     e = cudaMemcpyAsync(img + s0 * per_proj, img_host + s0 * per_proj, (size_t)(s1 - s0) * per_proj * 4,
@@ -923,19 +936,20 @@ int cbp_backproject_host_f32(const float* img_host, int64_t np, int64_t nh, int6
     if (e == cudaSuccess) e = cudaEventRecord(ev_proj[q], sc);
     if (e != cudaSuccess) rc = cuda_fail(e, "host path: projection upload");
   }
-  for (int64_t k = 1; k < n_slabs && rc == CBP_OK; ++k)
-    if ((e = up_slab(k)) != cudaSuccess) rc = cuda_fail(e, "host path: volume upload");
-  // compute: slab 0 follows the projection chunks as they land, the others run over all angles
-  for (int64_t k = 0; k < n_slabs && rc == CBP_OK; ++k) {
+  for (int64_t t = 1; t < n_slabs && rc == CBP_OK; ++t)
+    if ((e = up_slab(order[t])) != cudaSuccess) rc = cuda_fail(e, "host path: volume upload");
+  // compute: the first slab follows the projection chunks as they land, the others run over all angles
+  for (int64_t t = 0; t < n_slabs && rc == CBP_OK; ++t) {
+    const int64_t k = order[t];
     if ((e = cudaStreamWaitEvent(sk, ev_vol[k], 0)) != cudaSuccess) {
       rc = cuda_fail(e, "host path: wait");
       break;
     }
     const int64_t k0 = zb[k], k1 = zb[k + 1];
     float* vslab = vol + (size_t)k0 * slice;
-    for (int64_t q = 0; q < (k == 0 ? n_chunks : 1) && rc == CBP_OK; ++q) {
-      const int64_t s0 = k == 0 ? np * q / n_chunks : 0, s1 = k == 0 ? np * (q + 1) / n_chunks : np;
-      if (k == 0) {
+    for (int64_t q = 0; q < (t == 0 ? n_chunks : 1) && rc == CBP_OK; ++q) {
+      const int64_t s0 = t == 0 ? np * q / n_chunks : 0, s1 = t == 0 ? np * (q + 1) / n_chunks : np;
+      if (t == 0) {
         if ((e = cudaStreamWaitEvent(sk, ev_proj[q], 0)) != cudaSuccess) {
           rc = cuda_fail(e, "host path: wait");
           break;
