@@ -156,21 +156,24 @@ __global__ void __launch_bounds__(256) fdk_filter_kernel(const float* __restrict
       for (int bf = tid; bf < N / 8; bf += T) {
         const int j = bf & (S - 1);
         const int base = ((bf >> (LOGL - 3)) << LOGL) + j;
+        // padded positions of the butterfly's 8 elements: a constant stride when S >= 16
+        const int p0 = P(base);
+        auto Q = [&](int m) { return S >= 16 ? p0 + m * (S + (S >> 4)) : P(base + m * S); };
         float2 x[8];
 #pragma unroll
-        for (int m = 0; m < 8; ++m) x[m] = (s == 0) ? load_in(base + m * S) : sm[P(base + m * S)];
+        for (int m = 0; m < 8; ++m) x[m] = (s == 0) ? load_in(base + m * S) : sm[Q(m)];
         dft_small<8, false>(x);
         const float2 w1 = __ldg(tw + ((size_t)j << (LOGN - LOGL)));
         const float2 w2 = cmul(w1, w1), w3 = cmul(w2, w1), w4 = cmul(w2, w2);
         const float2 w5 = cmul(w4, w1), w6 = cmul(w3, w3), w7 = cmul(w4, w3);
-        sm[P(base)] = x[0];
-        sm[P(base + S)] = cmul(x[1], w1);
-        sm[P(base + 2 * S)] = cmul(x[2], w2);
-        sm[P(base + 3 * S)] = cmul(x[3], w3);
-        sm[P(base + 4 * S)] = cmul(x[4], w4);
-        sm[P(base + 5 * S)] = cmul(x[5], w5);
-        sm[P(base + 6 * S)] = cmul(x[6], w6);
-        sm[P(base + 7 * S)] = cmul(x[7], w7);
+        sm[Q(0)] = x[0];
+        sm[Q(1)] = cmul(x[1], w1);
+        sm[Q(2)] = cmul(x[2], w2);
+        sm[Q(3)] = cmul(x[3], w3);
+        sm[Q(4)] = cmul(x[4], w4);
+        sm[Q(5)] = cmul(x[5], w5);
+        sm[Q(6)] = cmul(x[6], w6);
+        sm[Q(7)] = cmul(x[7], w7);
       }
       __syncthreads();
     }
@@ -203,20 +206,22 @@ __global__ void __launch_bounds__(256) fdk_filter_kernel(const float* __restrict
         const float2 w1 = __ldg(tw + ((size_t)j << (LOGN - LOGL)));
         const float2 w2 = cmul(w1, w1), w3 = cmul(w2, w1), w4 = cmul(w2, w2);
         const float2 w5 = cmul(w4, w1), w6 = cmul(w3, w3), w7 = cmul(w4, w3);
+        const int p0 = P(base);
+        auto Q = [&](int m) { return S >= 16 ? p0 + m * (S + (S >> 4)) : P(base + m * S); };
         float2 x[8];
-        x[0] = sm[P(base)];
-        x[1] = cmulc(sm[P(base + S)], w1);
-        x[2] = cmulc(sm[P(base + 2 * S)], w2);
-        x[3] = cmulc(sm[P(base + 3 * S)], w3);
-        x[4] = cmulc(sm[P(base + 4 * S)], w4);
-        x[5] = cmulc(sm[P(base + 5 * S)], w5);
-        x[6] = cmulc(sm[P(base + 6 * S)], w6);
-        x[7] = cmulc(sm[P(base + 7 * S)], w7);
+        x[0] = sm[Q(0)];
+        x[1] = cmulc(sm[Q(1)], w1);
+        x[2] = cmulc(sm[Q(2)], w2);
+        x[3] = cmulc(sm[Q(3)], w3);
+        x[4] = cmulc(sm[Q(4)], w4);
+        x[5] = cmulc(sm[Q(5)], w5);
+        x[6] = cmulc(sm[Q(6)], w6);
+        x[7] = cmulc(sm[Q(7)], w7);
         dft_small<8, true>(x);
 #pragma unroll
         for (int m = 0; m < 8; ++m) {
           if (s == 0) store_out(base + m * S, x[m]);
-          else sm[P(base + m * S)] = x[m];
+          else sm[Q(m)] = x[m];
         }
       }
       if (s != 0) __syncthreads();
