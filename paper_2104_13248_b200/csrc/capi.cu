@@ -214,7 +214,8 @@ const void* tiled_kernel_ptr_c(int variant, bool gen, int c) {
 #endif
 const void* tiled_kernel_ptr(int variant, bool gen, int c, bool check) {
 #if CBP_DEV_SLIM  // kernel-tuning builds: only the baseline fast-path instances of tile shapes 0 and 1 (seconds to compile)
-  (void)variant; (void)gen; (void)check;
+  (void)variant; (void)check;
+  if (gen) return tiled_fn<V_BASELINE, true, 1, false>();
   return c == 1   ? tiled_fn<V_BASELINE, false, 1, false>()
          : c == 3 ? tiled_fn<V_BASELINE, false, 3, false>()
                   : tiled_fn<V_BASELINE, false, 0, false>();
@@ -676,7 +677,7 @@ int launch_staged(StagedCall c, unsigned long long* stats, cudaStream_t st) {
   }
   const void* fn =
 #if CBP_DEV_SLIM
-      tiled_kernel_ptr(key.variant, false, plan.cfg, false);
+      tiled_kernel_ptr(key.variant, plan.kind == 2, plan.cfg, false);
 #else
       (c.flags & CBP_FLAG_FMA_LERP)
                        ? (plan.kind == 2 ? fmalerp_by_tile<true>(plan.cfg) : fmalerp_by_tile<false>(plan.cfg))
@@ -702,7 +703,8 @@ int launch_staged(StagedCall c, unsigned long long* stats, cudaStream_t st) {
   p.ty_const = c.nz <= kTyTabMax ? 1 : 0;
   // the same loop forms texel byte addresses with one subnormal FMA (bp_kernels.cuh, ADDR_W4):
   // exact while |box base - v0 * row pitch| < 2^24
-  if (c.nh * (int64_t)plan.wb * 4 >= (1 << 24) - (1 << 19)) p.ty_const = 0;
+  p.addr_ok = c.nh * (int64_t)plan.wb * 4 < (1 << 24) - (1 << 19) ? 1 : 0;
+  if (!p.addr_ok) p.ty_const = 0;
   {
     uint32_t m6_bits;
     std::memcpy(&m6_bits, c.mats_host + 12 * c.s_begin + 6, 4);

@@ -63,16 +63,21 @@ def test_device_entry_points_fail_loudly_without_gpu():
 def test_no_fma_contraction_in_backprojection_sass():
     """Bit-exactness needs separately rounded products and sums: the SASS of the
     back-projection kernels must contain no fused multiply-add on sample values.  The only
-    FFMA2 allowed is the texel ADDRESS of the guard-free loop (floor(y) * row pitch + base on
-    subnormal floats, exact by construction: bp_kernels.cuh hot_loop): one per slice pair,
-    recognisable by its broadcast scalar operands: row pitch as multiplier and, above all, the
-    base address as ADDEND -- every sum of the sample arithmetic adds a packed pair.  (Scalar
-    FFMA are the explicit Newton steps of the correctly rounded reciprocal.)"""
+    FFMA2 allowed are the texel ADDRESSES of the guard-free loops (floor * pitch + base on
+    subnormal floats, exact by construction: bp_kernels.cuh hot_loop / gen_loop): one per slice
+    pair on the fast path (multiplier and addend broadcast scalars), two on the general path
+    (fx * 4 + base, then fy * pitch + that), every multiplier a broadcast scalar.  A contraction
+    of the sample arithmetic would add several FFMA2 per slice pair (ten mul+add pairs in the
+    blend), so the COUNT per kernel is checked as well.  (Scalar FFMA are the explicit Newton
+    steps of the correctly rounded reciprocal.)"""
     out = subprocess.run(["cuobjdump", "-sass", str(_lib.LIB_PATH)], capture_output=True, text=True)
     if out.returncode != 0:
         pytest.skip("cuobjdump unavailable")
     funcs = re.split(r"\n\s+Function : ", out.stdout)
-    addr_fma = re.compile(r"FFMA2 R\d+, R\d+(\.reuse)?\.F32x2\.LO_HI, U?R\d+(\.reuse)?\.F32, R\d+(\.reuse)?\.F32 ;")
+    reg = r"R\d+(\.reuse)?"
+    mult = rf"(U?{reg}\.F32|5\.605\d+e-45)"  # broadcast row pitch, or the immediate 4 * 2^-149 (x step in bytes)
+    addr_fma = re.compile(rf"FFMA2 R\d+, {reg}\.F32x2\.LO_HI, {mult}, {reg}\.F32(x2\.(LO_HI|HI_LO))? ;")
+    fast_form = re.compile(rf"FFMA2 R\d+, {reg}\.F32x2\.LO_HI, {mult}, {reg}\.F32 ;")
     checked = with_addr = 0
     for f in funcs:
         name = f.split("\n", 1)[0]
@@ -80,8 +85,12 @@ def test_no_fma_contraction_in_backprojection_sass():
             checked += 1
             fused = [ln for ln in f.split("\n") if "FFMA2" in ln]
             assert all(addr_fma.search(ln) for ln in fused), (name, [ln for ln in fused if not addr_fma.search(ln)][:3])
-            # one guard-free loop per kernel at most: 16 slice pairs (8 in the half z-run kernels)
-            assert len(fused) in (0, 8, 16), (name, len(fused))
+            # 16 slice pairs per guard-free loop (8 in the half z-run kernels), one address FMA per
+            # pair on the fast path, two on the general path
+            assert len(fused) in (0, 8, 16, 32), (name, len(fused))
+            # at least half of them have the fast path's all-broadcast form (the general path's
+            # second FMA adds the packed result of its first)
+            assert 2 * sum(bool(fast_form.search(ln)) for ln in fused) >= len(fused), name
             with_addr += bool(fused)
         if "bp_tiled_fmalerp_kernel" in name:  # the opt-in tolerance mode does fuse its lerps
             assert "FFMA2" in f, name
