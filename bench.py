@@ -282,8 +282,12 @@ def run_reference(args, spec, geom, mats) -> None:
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": spec.inputs + " (synthetic, seeded; the same bytes as --impl ours)",
-            "config": spec.describe() | {"variant": "baseline", "sample_slices": nk,
-                                         "same_config": nk == geom.nz},
+            # the same workload as --impl ours; a step covers a bounded sample of it (the contract's
+            # "bounded sample of that workload"), described here and in cpu_baseline.sample
+            "config": spec.describe() | {"variant": "baseline", "parallelism": f"host threads x{threads}",
+                                         "arithmetic": "bit-exact (reference float32 op order)",
+                                         "step_sample": {"z_slices": nk, "of": geom.nz,
+                                                         "whole_volume": nk == geom.nz}},
             "cpu_baseline": {"value": value, "unit": "GUPS", "cores": threads, "kind": kind,
                              "sample": f"per step: {sample}; {desc}, {threads} threads"},
             "e2e": {"value": value, "unit": "GUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
