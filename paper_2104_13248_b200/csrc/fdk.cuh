@@ -13,8 +13,8 @@
 //
 //   * two real rows a, b ride one complex transform z = a + i b: the Ram-Lak spectrum H is
 //     real and even, so IFFT(H FFT(z)) = a*h + i (b*h);
-//   * the transform lives in shared memory (N complex, padded 1 in 16 against bank
-//     conflicts): decimation-in-frequency radix-8 passes forward, leaving the spectrum in
+//   * the transform lives in shared memory (N complex; index swizzle or 1-in-16 padding against
+//     bank conflicts): decimation-in-frequency radix-8 passes forward, leaving the spectrum in
 //     digit-reversed order; H is stored in that order (host table), so no reordering pass
 //     exists; the inverse runs the same passes backwards (decimation in time) and lands
 //     in natural order;
@@ -114,7 +114,15 @@ __global__ void __launch_bounds__(256) fdk_filter_kernel(const float* __restrict
   constexpr int RM = 1 << (LOGN - 3 * A);     // innermost radix (8, 4 or 2)
   extern __shared__ float2 fdk_sm[];
   float2* sm = fdk_sm;
-  auto P = [](int i) { return i + (i >> 4); };  // 1 pad element per 16
+  // Position of element i in shared memory (float2 = one bank pair, 16 pairs per wavefront).
+  // The passes touch three patterns per half-warp: 16 consecutive elements; two blocks of 8
+  // consecutive elements 64 apart (the stride-8 pass); 16 elements 8 apart (the innermost pass).
+  // For transforms whose innermost radix is 8 (N = 64, 512, 4096) an XOR swizzle of the low four
+  // index bits with bits 4..6 (and bit 6 again into bit 3) makes all three conflict free
+  // (ncu: the 1-in-16 padding left 26% conflict wavefronts on N = 4096, all from the stride-8
+  // pass); the other lengths keep the padding.
+  constexpr bool SWZ = (RM == 8) && LOGN >= 6;
+  auto P = [](int i) { return SWZ ? (i ^ (((i >> 4) & 7) | (((i >> 6) & 1) << 3))) : i + (i >> 4); };
   const int tid = threadIdx.x, T = blockDim.x;
   const long long pairs = (rows + 1) >> 1;
   for (long long pr = blockIdx.x; pr < pairs; pr += gridDim.x) {
@@ -158,7 +166,10 @@ __global__ void __launch_bounds__(256) fdk_filter_kernel(const float* __restrict
         const int base = ((bf >> (LOGL - 3)) << LOGL) + j;
         // padded positions of the butterfly's 8 elements: a constant stride when S >= 16
         const int p0 = P(base);
-        auto Q = [&](int m) { return S >= 16 ? p0 + m * (S + (S >> 4)) : P(base + m * S); };
+        auto Q = [&](int m) {
+          if (SWZ) return S >= 128 ? p0 + m * S : P(base + m * S);  // the swizzle reads index bits 4..6
+          return S >= 16 ? p0 + m * (S + (S >> 4)) : P(base + m * S);
+        };
         float2 x[8];
 #pragma unroll
         for (int m = 0; m < 8; ++m) x[m] = (s == 0) ? load_in(base + m * S) : sm[Q(m)];
@@ -207,7 +218,10 @@ __global__ void __launch_bounds__(256) fdk_filter_kernel(const float* __restrict
         const float2 w2 = cmul(w1, w1), w3 = cmul(w2, w1), w4 = cmul(w2, w2);
         const float2 w5 = cmul(w4, w1), w6 = cmul(w3, w3), w7 = cmul(w4, w3);
         const int p0 = P(base);
-        auto Q = [&](int m) { return S >= 16 ? p0 + m * (S + (S >> 4)) : P(base + m * S); };
+        auto Q = [&](int m) {
+          if (SWZ) return S >= 128 ? p0 + m * S : P(base + m * S);  // the swizzle reads index bits 4..6
+          return S >= 16 ? p0 + m * (S + (S >> 4)) : P(base + m * S);
+        };
         float2 x[8];
         x[0] = sm[Q(0)];
         x[1] = cmulc(sm[Q(1)], w1);
