@@ -1198,6 +1198,13 @@ int cbp_slab_plan(const float* mats_host, int64_t np, int64_t nh, int64_t nw, in
   // 32x16-column tiles and angles.  (A per-voxel sampled count under-weights the
   // partially sampled tiles at the volume's z ends: 0.78 instead of 0.97 compute balance
   // on cfg4 at 8 ranks, tools/slab_balance.py.)
+  // Weights fitted to the per-rank times of tools/slab_balance.py (round 2): on the fast path a
+  // tile crossing the detector's top or bottom row costs 1.15x (its columns check u once per
+  // angle anyway); on the general path (per-voxel 1/z and x) the guard-free loop needs the whole
+  // tile on the detector in u and v, and a guarded pair costs 2x; a never-queued pair costs the
+  // producer's footprint test.
+  const bool gen = !fast_path_ok(mats_host, np, variant);
+  const double w_guard = gen ? 2.0 : 1.15, w_miss = gen ? 0.06 : 0.03;
   const int64_t TXm = 32, TYm = 16;
   const int64_t ntx = ceil_div(nx, TXm), nty = ceil_div(ny, TYm);
   const int64_t stx = std::max<int64_t>(1, ntx / 12), sty = std::max<int64_t>(1, nty / 12);
@@ -1228,9 +1235,10 @@ int cbp_slab_plan(const float* mats_host, int64_t np, int64_t nh, int64_t nw, in
           const double vlo = std::floor(vmin) - 1, vhi = std::floor(vmax_) + 1;
           const bool hit = std::max(ulo, 0.0) <= std::min(uhi, (double)(nw - 2)) &&
                            std::max(vlo, 0.0) <= std::min(vhi, (double)(nh - 2));
-          if (!hit) { c += 0.03; continue; }
+          if (!hit) { c += w_miss; continue; }
           const bool rows_inside = vlo >= 0 && vhi <= (double)(nh - 2);
-          c += rows_inside ? 1.0 : 1.15;
+          const bool cols_inside = ulo >= 0 && uhi <= (double)(nw - 2);
+          c += (rows_inside && (cols_inside || !gen)) ? 1.0 : w_guard;
         }
     cost[L] = c * (double)(kb - ka + 1) / (double)align + 1e-9;
   }
