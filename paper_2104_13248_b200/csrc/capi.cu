@@ -1297,8 +1297,21 @@ int cbp_forward_project_f32(const float* vol_dev, int64_t nx, int64_t ny, int64_
   double* vd = nullptr;
   CK(cudaMallocAsync(reinterpret_cast<void**>(&vd), (size_t)np * 12 * sizeof(double), st), "alloc views");
   CK(cudaMemcpyAsync(vd, views_host, (size_t)np * 12 * sizeof(double), cudaMemcpyHostToDevice, st), "upload views");
+  // a copy of the volume with y contiguous for the rays that run mostly along x (fwd_kernels.cuh);
+  // without the memory for it every ray reads the natural layout
+  float* vol_t = nullptr;
+  const bool want_t = std::getenv("CBP_FWD_NATURAL_ONLY") == nullptr;  // measurement knob (tools/time_f1_f2.py)
+  if (want_t && nz <= 65535 &&
+      cudaMallocAsync(reinterpret_cast<void**>(&vol_t), (size_t)nx * ny * nz * sizeof(float), st) == cudaSuccess) {
+    dim3 b(32, 8), g((unsigned)ceil_div(ny, 32), (unsigned)ceil_div(nx, 32), (unsigned)nz);
+    // out[z][x][y] = vol[z][y][x]: the staging transpose with (u, v) = (y, x)
+    stage_transposed_kernel<<<g, b, 0, st>>>(vol_dev, (int)nx, (int)ny, 0, (int)nx, vol_t, (int)ny);
+  } else {
+    cudaGetLastError();  // clear the failed allocation
+    vol_t = nullptr;
+  }
   FwdParams fp;
-  fp.vol = vol_dev; fp.views = vd; fp.out = out_dev;
+  fp.vol = vol_dev; fp.vol_t = vol_t; fp.views = vd; fp.out = out_dev;
   fp.np = (int)np; fp.nh = (int)nh; fp.nw = (int)nw; fp.nx = (int)nx; fp.ny = (int)ny; fp.nz = (int)nz;
   fp.pu = pixel_pitch_u; fp.pv = pixel_pitch_v; fp.cu = cu; fp.cv = cv; fp.s = voxel_size;
   const int64_t rays = np * nh * nw;
@@ -1310,6 +1323,7 @@ int cbp_forward_project_f32(const float* vol_dev, int64_t nx, int64_t ny, int64_
     bp_forward_kernel<false><<<(unsigned)ceil_div(rays, 256), 256, 0, st>>>(fp);
   cudaError_t e = cudaGetLastError();
   cudaFreeAsync(vd, st);
+  if (vol_t) cudaFreeAsync(vol_t, st);
   if (e != cudaSuccess) return cuda_fail(e, "forward kernel launch");
   return CBP_OK;
 }

@@ -19,6 +19,7 @@ __device__ __forceinline__ double dd(double a, double b) { return __ddiv_rn(a, b
 
 struct FwdParams {
   const float* vol;      // [nz][ny][nx]
+  const float* vol_t;    // the same volume as [nz][nx][ny] (y contiguous), or null
   const double* views;   // [np][12]: source xyz, detector-centre xyz, e_u xyz, e_v xyz
   float* out;            // [np][nh][nw]
   int np, nh, nw, nx, ny, nz;
@@ -26,6 +27,12 @@ struct FwdParams {
 };
 
 // One ray per thread (phantom.py:145-221).
+// The lanes of a warp are neighbouring detector columns: their sample points lie on a line
+// across the ray in the xy-plane.  For rays that run mostly along y that line runs along x and
+// a warp-wide gather touches a few 32-byte sectors of one volume row; for rays mostly along x
+// it touched a different row per lane (ncu: the L1 data pipe 99% busy, 14 wavefronts per
+// gather on average).  Those rays read a copy of the volume with y contiguous instead
+// (p.vol_t): the same eight voxels, the same arithmetic, a third of the wavefronts.
 // POW2: the voxel size is a power of two (1.0 in every BASELINE config), so the three float64
 // divisions by it per ray step are multiplications by its exact reciprocal -- the same
 // correctly rounded quotient, a third of the float64 work per step.
@@ -57,6 +64,10 @@ __global__ void __launch_bounds__(256) bp_forward_kernel(const FwdParams p) {
   dz = dd(dz, norm);
   double t0 = 0.0, t1 = norm;
   float* o = p.out + flat;
+  // which copy of the volume this ray reads, and its element strides in x and y
+  const bool tr = p.vol_t != nullptr && fabs(dx) > fabs(dy);
+  const float* __restrict__ vbase = tr ? p.vol_t : p.vol;
+  const long long sx_ = tr ? p.ny : 1, sy_ = tr ? 1 : p.nx, sz_ = (long long)p.nx * p.ny;
   // slab intersection with the voxel-centre box (phantom.py:164-192)
   if (dx != 0.0) {
     const double ta = dd(ds(-hx, sx), dx), tb = dd(ds(hx, sx), dx);
@@ -103,15 +114,15 @@ __global__ void __launch_bounds__(256) bp_forward_kernel(const FwdParams p) {
     if (iy > p.ny - 2) iy = p.ny - 2;
     if (iz > p.nz - 2) iz = p.nz - 2;
     const double ax = ds(fx, (double)ix), ay = ds(fy, (double)iy), az = ds(fz, (double)iz);
-    const float* v00 = p.vol + ((long long)iz * p.ny + iy) * p.nx + ix;
-    const float* v10 = v00 + p.nx;
-    const float* v01 = v00 + (long long)p.nx * p.ny;
-    const float* v11 = v01 + p.nx;
+    const float* v00 = vbase + iz * sz_ + iy * sy_ + ix * sx_;  // voxel (ix, iy, iz)
+    const float* v10 = v00 + sy_;                                // (ix, iy + 1, iz)
+    const float* v01 = v00 + sz_;                                // (ix, iy, iz + 1)
+    const float* v11 = v01 + sy_;                                // (ix, iy + 1, iz + 1)
     const double oax = ds(1.0, ax), oay = ds(1.0, ay), oaz = ds(1.0, az);
-    const double c00 = da(dm((double)__ldg(v00), oax), dm((double)__ldg(v00 + 1), ax));
-    const double c10 = da(dm((double)__ldg(v10), oax), dm((double)__ldg(v10 + 1), ax));
-    const double c01 = da(dm((double)__ldg(v01), oax), dm((double)__ldg(v01 + 1), ax));
-    const double c11 = da(dm((double)__ldg(v11), oax), dm((double)__ldg(v11 + 1), ax));
+    const double c00 = da(dm((double)__ldg(v00), oax), dm((double)__ldg(v00 + sx_), ax));
+    const double c10 = da(dm((double)__ldg(v10), oax), dm((double)__ldg(v10 + sx_), ax));
+    const double c01 = da(dm((double)__ldg(v01), oax), dm((double)__ldg(v01 + sx_), ax));
+    const double c11 = da(dm((double)__ldg(v11), oax), dm((double)__ldg(v11 + sx_), ax));
     const double lo = da(dm(c00, oay), dm(c10, ay));
     const double hi = da(dm(c01, oay), dm(c11, ay));
     total_sum = da(total_sum, dm(da(dm(lo, oaz), dm(hi, az)), step));

@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -79,7 +80,8 @@ def main():
         # f2 on the config's grid (bounded: cfg3 is 1024^3 x 1440 x 1536^2 rays -> time a subset of angles)
         n_sub = min(n_proj, 32)
         vol = torch.rand((geom.nz, geom.ny, geom.nx), device="cuda")
-        views = _views_array(circular_views(geom)[:n_sub])
+        all_views = circular_views(geom)
+        views = _views_array(all_views[::max(1, len(all_views) // n_sub)][:n_sub])  # evenly spaced over the orbit
         r2 = None
         if not args.skip_f2:
             outp = torch.empty((n_sub, nh, nw), device="cuda")
@@ -92,9 +94,14 @@ def main():
                     stream_handle()))
 
             ms2 = timed(f2, iters=2)
+            os.environ["CBP_FWD_NATURAL_ONLY"] = "1"  # every ray reads the natural layout (round-2 first version)
+            ms2_nat = timed(f2, iters=2)
+            del os.environ["CBP_FWD_NATURAL_ONLY"]
             rays = n_sub * nh * nw
-            r2 = {"ms": ms2, "angles_timed": n_sub, "rays_per_s": rays / ms2 / 1e-3,
-                  "note": "float64 ray marching (bitwise equal to the reference's numba _forward)"}
+            r2 = {"ms": ms2, "ms_natural_layout_only": ms2_nat, "angles_timed": n_sub,
+                  "angles": "evenly spaced over the orbit", "rays_per_s": rays / ms2 / 1e-3,
+                  "note": "float64 ray marching (bitwise equal to the reference's numba _forward); rays that run "
+                          "mostly along x read a y-contiguous copy of the volume (transpose inside the timed call)"}
         out[spec.name] = {"f1_fdk_filter": r1, "f2_forward_projector": r2}
         print(json.dumps({spec.name: out[spec.name]}), flush=True)
         del vol
